@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark of the GVR exact Top-K hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl gvr|radix|reference]
+
+A *step* is one pass of the whole hot path over one batch: one gvr_topk_batched launch
+over all rows of the workload (BASELINE.json configs).  The default workload is
+configs[1] (cfg2): 8 requests x 61 layers = 488 rows of N = 100,000 fp32 indexer
+scores (Eq. 1, synthetic, prev-step guesses), K = 2048.  Inputs are resident
+in HBM before the timed region; three distinct batches are rotated so every step reads
+cold data (3 x 195 MB > 126 MB L2).  Rank 0 prints one JSON line.
+
+Under torchrun (N > 1) every rank processes its own batch of the same shape (rows are
+independent; no collective on the hot path) — weak scaling; the elapsed time is the
+max over ranks.  --impl reference times the CPU oracle on the host (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K = 2048
+CONFIGS = {
+    "cfg1": dict(requests=1, layers=1, n=8192, draft=1, desc="single decode row N=8192"),
+    "cfg2": dict(requests=8, layers=61, n=100_000, draft=1, desc="batch 8 x 61 layers, N=100K"),
+    "cfg3": dict(requests=1, layers=1, n=131_072, draft=1, desc="batch-1 long context"),
+    "cfg4": dict(requests=16, layers=61, n=100_000, draft=4, desc="MTP-3: 16 requests x 4 tokens x 61 layers"),
+    "cfg5": dict(requests=64, layers=61, n=131_072, draft=1, desc="64 requests x 61 layers, N=128K"),
+}
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+# ----------------------------------------------------------------------------- inputs
+def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0):
+    """Synthetic decode batch: rows (request, layer, draft j) of length n + j from the
+    Eq. 1 indexer (synth.IndexerLayer), plus prev_topk = the exact Top-K of the
+    request's previous step (n - 1 keys), shared by its draft rows.
+    The previous step's Top-K is computed with the GVR kernel itself (no guess), i.e.
+    the decode loop feeding its own output back; it is only a hint."""
+    import torch
+
+    import paper_2604_22312_b200 as gvr
+    import synth
+
+    R = requests * layers * draft
+    S = n + draft - 1
+    scores = torch.zeros((R, S), dtype=torch.float32, device=dev)
+    lens = torch.empty(R, dtype=torch.int32)
+    prev_rows = torch.zeros((requests * layers, S), dtype=torch.float32, device=dev)
+    row = 0
+    for q in range(requests):
+        for l in range(layers):
+            s = synth.splitmix64(seed, rank, q, l)
+            lay = synth.IndexerLayer(S, synth.layer_rho(l, seed), s, dev)
+            prev_rows[q * layers + l, :n - 1] = lay.scores(n - 1)
+            lay.step()
+            for j in range(draft):
+                scores[row, :n + j] = lay.scores(n + j)
+                lens[row] = n + j
+                row += 1
+            del lay
+    plens = torch.full((requests * layers,), n - 1, dtype=torch.int32, device=dev)
+    ptop = gvr.topk(prev_rows, K, row_lens=plens)
+    prev = ptop.repeat_interleave(draft, dim=0).contiguous()
+    del prev_rows
+    return {"scores": scores, "row_lens": lens.to(dev), "prev": prev, "R": R, "n": n}
+
+
+def algorithmic_bytes(lens, k=K):
+    """Bytes the method must move per launch: each row read once (4N), the guess read
+    (4K), the output written (4K) and the row length (4) — SURVEY.md 8(d) B(N)."""
+    return int(4 * int(np.sum(lens)) + len(lens) * (4 * k + 4 * k + 4))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (clock + throttle reasons)."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, name in REASON_BITS.items():
+                if bits & b:
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- timing
+def time_steps(fn, batches, steps, warmup, stream):
+    import torch
+    for i in range(warmup):
+        fn(batches[i % len(batches)])
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(steps):
+        fn(batches[i % len(batches)])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    return ev0.elapsed_time(ev1) / 1e3  # seconds
+
+
+def cpu_oracle_rate(host_scores, lens, max_rows=None, threads=None):
+    import oracle
+    rows = host_scores if max_rows is None else host_scores[:max_rows]
+    ln = lens if max_rows is None else lens[:max_rows]
+    threads = threads or os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.topk_batched(rows, K, row_lens=ln, num_threads=threads)
+    dt = time.perf_counter() - t0
+    return rows.shape[0] / dt, threads, rows.shape[0], dt
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="gvr", choices=["gvr", "radix", "reference"])
+    ap.add_argument("--nbatches", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--check", action="store_true", help="verify every batch against the oracle")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2604_22312_b200 as gvr
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    batches = [make_decode_batch(cfg["requests"], cfg["layers"], cfg["n"], dev,
+                                 seed=synth.splitmix64(synth.BASE_SEED, b), draft=cfg["draft"], rank=rank)
+               for b in range(args.nbatches)]
+    torch.cuda.synchronize()
+    R = batches[0]["R"]
+    lens_np = batches[0]["row_lens"].cpu().numpy()
+    stream = torch.cuda.current_stream()
+    for b in batches:
+        b["out"] = torch.empty((R, K), dtype=torch.int32, device=dev)
+
+    def gvr_step(b):
+        gvr.topk(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"])
+
+    def radix_step(b):
+        gvr.radix_topk(b["scores"], K, row_lens=b["row_lens"], out=b["out"])
+
+    main_fn = gvr_step if args.impl == "gvr" else radix_step
+    other_fn = radix_step if args.impl == "gvr" else gvr_step
+
+    # correctness gate (oracle) on one batch before timing
+    check = {}
+    if rank == 0:
+        import oracle
+        b0 = batches[0]
+        main_fn(b0)
+        torch.cuda.synchronize()
+        host0 = b0["scores"].cpu().numpy()
+        ref = oracle.topk_batched(host0, K, row_lens=lens_np)
+        ok = bool(np.array_equal(b0["out"].cpu().numpy(), ref))
+        check = {"bit_exact_vs_oracle": ok, "rows_checked": int(R)}
+        if not ok:
+            print(json.dumps({"error": "parity failure vs oracle", "config": args.config}), flush=True)
+            sys.exit(2)
+
+    # timed region
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    phys = vis.split(",")[local_rank] if vis else str(local_rank)
+    with ClockSampler(phys) as clk:
+        elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream)
+    if dist is not None:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    ms_per_step = elapsed / args.steps * 1e3
+    rows_total = R * world * args.steps
+    value = rows_total / elapsed
+
+    # the other kernel, same protocol (speedup vs own radix select)
+    other_elapsed = time_steps(other_fn, batches, args.steps, args.warmup, stream)
+    if dist is not None:
+        t = torch.tensor([other_elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        other_elapsed = float(t.item())
+
+    # per-row stats (passes etc.) on one batch, outside the timed region
+    b0 = batches[0]
+    if args.impl == "gvr":
+        _, _, st = gvr.topk_ex(b0["scores"], K, row_lens=b0["row_lens"], prev=b0["prev"], values=False)
+    else:
+        _, _, st = gvr.radix_topk_ex(b0["scores"], K, row_lens=b0["row_lens"], values=False)
+    st = st.cpu().numpy()
+
+    result = None
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        abytes = algorithmic_bytes(lens_np)
+        kern_s = elapsed / args.steps  # one launch per step
+        achieved = abytes / kern_s / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get(f"{args.impl}_{args.config}")
+            except Exception:
+                traffic = None
+        gvr_t = elapsed if args.impl == "gvr" else other_elapsed
+        rad_t = other_elapsed if args.impl == "gvr" else elapsed
+        result = {
+            "metric": "µs/row & rows/s, K=2048 N=100K; speedup vs own radix-select; HBM GB/s",
+            "value": round(value, 1),
+            "unit": "rows/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (PAPER.md Eq. 1 indexer rows, YaRN RoPE, AR(1) decode steps; prev-step Top-K guesses)",
+            "impl": args.impl,
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "rows_per_gpu": R, "N": cfg["n"], "K": K,
+                       "draft_tokens": cfg["draft"], "parallelism": f"row-shard x{world}",
+                       "l2": f"inputs larger than L2: {args.nbatches} distinct batches rotated "
+                             f"({args.nbatches * R * (cfg['n'] + cfg['draft'] - 1) * 4 / 1e6:.0f} MB)"},
+            "us_per_row": round(elapsed / (R * args.steps) * 1e6, 5),
+            "speedup_vs_radix": round(rad_t / gvr_t, 3),
+            "radix_rows_per_s": round(R * world * args.steps / rad_t, 1),
+            "hbm_gbs": round(achieved, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": abytes,
+                         "kernel": "gvr_topk_kernel" if args.impl == "gvr" else "radix_topk_kernel"},
+            "passes_per_row": {"global_mean": float(st[:, 4].mean()), "secant_mean": float(st[:, 0].mean()),
+                               "snap_mean": float(st[:, 1].mean()), "raises_mean": float(st[:, 5].mean()),
+                               "cand_mean": float(st[:, 2].mean())},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "check": check,
+        }
+    # end-to-end through the host-buffer C ABI (H2D + kernel + D2H in the timed region)
+    if rank == 0 and not args.no_e2e and args.impl == "gvr":
+        result["e2e"] = run_e2e(gvr, batches[0], args, dev)
+    if rank == 0 and not args.no_cpu:
+        host0 = batches[0]["scores"].cpu().numpy()
+        rate, threads, nrows, dt = cpu_oracle_rate(host0, lens_np)
+        result["cpu_baseline"] = {"value": round(rate, 2), "unit": "rows/s", "cores": threads, "kind": "oracle",
+                                  "sample": f"{nrows} rows of {args.config} (one full batch), qsort oracle, "
+                                            f"{dt:.2f} s wall on {threads} threads"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(gvr, batch, args, dev):
+    import torch
+    R = batch["R"]
+    S = batch["scores"].shape[1]
+    h_scores = torch.empty((R, S), dtype=torch.float32, pin_memory=True)
+    h_scores.copy_(batch["scores"].cpu())
+    h_prev = torch.empty((R, K), dtype=torch.int32, pin_memory=True)
+    h_prev.copy_(batch["prev"].cpu())
+    h_lens = torch.empty(R, dtype=torch.int32, pin_memory=True)
+    h_lens.copy_(batch["row_lens"].cpu())
+    h_out = torch.empty((R, K), dtype=torch.int32, pin_memory=True)
+    ws = gvr.Workspace(R, S, K)
+    stream = torch.cuda.current_stream()
+    steps = max(3, min(args.steps, 10))
+
+    def step():
+        gvr.topk_host_ptr(h_scores.data_ptr(), S, R, ws, K, h_out.data_ptr(), prev_ptr=h_prev.data_ptr(),
+                          lens_ptr=h_lens.data_ptr(), stream=stream)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dt = ev0.elapsed_time(ev1) / 1e3
+    ws.close()
+    return {"value": round(R * steps / dt, 1), "unit": "rows/s",
+            "h2d_bytes_per_step": int(R * S * 4 + R * K * 4 + R * 4),
+            "d2h_bytes_per_step": int(R * K * 4), "steps": steps,
+            "api": "gvr_topk_batched_host (C ABI, pinned host buffers)"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores, rank 0 only.
+    Each step is a bounded sample of the workload (SAMPLE rows of the config)."""
+    if rank != 0:
+        return
+    import torch
+
+    import synth
+    torch.set_num_threads(os.cpu_count() or 1)
+    sample_rows = 16
+    n = cfg["n"]
+    rows, lens = [], []
+    r = 0
+    for l in range(cfg["layers"]):
+        if r >= sample_rows:
+            break
+        lay = synth.IndexerLayer(n + cfg["draft"] - 1, synth.layer_rho(l, synth.BASE_SEED),
+                                 synth.splitmix64(synth.BASE_SEED, 0, 0, l), "cpu")
+        lay.step()
+        for j in range(cfg["draft"]):
+            if r >= sample_rows:
+                break
+            row = np.zeros(n + cfg["draft"] - 1, np.float32)
+            row[:n + j] = lay.scores(n + j).numpy()
+            rows.append(row)
+            lens.append(n + j)
+            r += 1
+    host = np.stack(rows)
+    lens = np.array(lens, np.int32)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_oracle_rate(host, lens, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_oracle_rate(host, lens, threads=threads)
+    dt = time.perf_counter() - t0
+    value = host.shape[0] * args.steps / dt
+    sample = f"{host.shape[0]} rows of {args.config} per step (N={n}), qsort oracle on {threads} threads"
+    print(json.dumps({
+        "metric": "µs/row & rows/s, K=2048 N=100K; speedup vs own radix-select; HBM GB/s",
+        "value": round(value, 2), "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "N": n, "K": K},
+        "cpu_baseline": {"value": round(value, 2), "unit": "rows/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 2), "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

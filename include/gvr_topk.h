@@ -1,0 +1,143 @@
+/*
+ * gvr_topk.h — C ABI of the B200-native GVR exact Top-K library (libgvrtopk.so).
+ *
+ * Operation (PAPER.md = arXiv 2604.22312 source):
+ *   For each row r of a batch of fp32 score rows x (one DSA indexer score vector
+ *   I_t per decode query, Eq. 1, lines 78-85), return the indices of its
+ *   k largest values (exact Top-K, Sec. 4.1), ORDERED by score
+ *   descending and, among equal scores, by index ascending (BASELINE.json
+ *   north_star; the paper itself leaves ties non-deterministic).
+ *   Scores are compared through the sortable FP32 key: +0 ranks
+ *   above -0, +/-Inf are ordinary values, NaNs sort beyond +/-Inf by bit pattern.
+ *   gvr_topk_* use the previous decode step's Top-K as a guess (Guess-Verify-Refine,
+ *   PAPER.md Sec. 4.2, Phases 1-4); radix_topk_* is the distribution-agnostic
+ *   radix-select baseline of PAPER.md Sec. 2.2 (lines 125-148).  Both produce the
+ *   same bytes for the same input; the guess never changes the result.
+ *
+ * Conventions shared by every entry point:
+ *   - Device pointers are caller-owned CUDA device pointers.  The library allocates
+ *     nothing per call and keeps no reference after return (CUDA-Graph capturable;
+ *     the stable-address requirement of PAPER.md:1476-1482).
+ *   - Calls are stream-ordered on `stream` (0 = legacy default stream) and do not
+ *     synchronise the host, except gvr_topk_batched_host (documented below).
+ *   - Layout: scores is row-major [num_rows, row_stride] fp32; row r occupies
+ *     scores[r*row_stride .. r*row_stride + row_lens[r]).  Rows need not be 16-byte
+ *     aligned (row_stride may be any value >= 1).
+ *   - Output: out_idx is row-major [num_rows, k] int32.  For j < min(k, len):
+ *     out_idx[r*k+j] = j-th index of the row in (score desc, index asc) order; for
+ *     j >= len it is -1 (rows shorter than k are padded).
+ *   - Errors are reported synchronously before any launch:
+ *       GVR_ERR_INVALID_ARGUMENT: num_rows < 0, k < 1, row_stride < 1, a required
+ *         pointer is NULL while num_rows > 0, or prev_topk partially overlaps out_idx;
+ *       GVR_ERR_UNSUPPORTED: k > GVR_MAX_K, row_stride > INT32_MAX;
+ *       GVR_ERR_CUDA: the launch failed (cudaGetLastError() is consumed).
+ *     num_rows == 0 is a successful no-op.
+ *   - Device-side precondition 0 <= row_lens[r] <= row_stride; out-of-range lengths
+ *     are clamped into that range.
+ */
+#ifndef GVR_TOPK_H
+#define GVR_TOPK_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GVR_MAX_K 2048           /* K of DSA decode; k is 1..2048 */
+#define GVR_WINDOW_C 6144        /* MAX_CANDIDATES C of Lemma 1  */
+
+typedef enum {
+    GVR_OK = 0,
+    GVR_ERR_INVALID_ARGUMENT = 1,
+    GVR_ERR_UNSUPPORTED = 2,
+    GVR_ERR_CUDA = 3
+} gvr_status;
+
+/* How a row finished (gvr_row_stats.done_kind). */
+typedef enum {
+    GVR_DONE_TRIVIAL = 0,    /* len <= k: every element emitted, then -1 padding      */
+    GVR_DONE_CONVERGED = 1,  /* Phases 1-4 found K <= f(T) <= capacity */
+    GVR_DONE_TIEFILL = 2,    /* massive ties at the K-th value: ordered tie fill        */
+                             /* (PAPER.md:417-420 caveat; R13)               */
+    GVR_DONE_RADIX = 3       /* radix-select entry point (baseline)                     */
+} gvr_done_kind;
+
+/* Per-row statistics (optional output of the _ex entry point). Reported, not part of
+ * the result contract. */
+typedef struct {
+    int32_t secant_iters;   /* I: threshold evaluations f(T) (Phase 2)  */
+    int32_t snap_iters;     /* S: Phase-4 snap iterations          */
+    int32_t cand_count;     /* candidates collected in Phase 3 (|{x >= T}|)           */
+    int32_t done_kind;      /* gvr_done_kind                                          */
+    int32_t global_passes;  /* full-row reads of the row from global memory           */
+    int32_t raises;         /* mid-stream collect-threshold raises         */
+    int32_t buffer_count;   /* f(T_c): size of the streamed candidate buffer          */
+    int32_t cluster;        /* CTAs cooperating on the row                            */
+} gvr_row_stats;
+
+/* Tuning knobs; NULL selects the defaults.  None of them changes the result. */
+typedef struct {
+    float collect_sigma;      /* T_c = pmean - collect_sigma * sd(guess values); default 0.5 */
+    int32_t max_secant_iters; /* secant steps before pure bisection; default 8              */
+    int32_t force_cluster;    /* 0 = automatic; else CTAs per row (1,2,4,8)                */
+    int32_t reserved;
+} gvr_options;
+
+/* GVR exact Top-K.  prev_topk: nullable device int32 [num_rows, k], the previous
+ * step's Top-K.  Entries may be any int32: negative,
+ * >= len, duplicated or all -1 are tolerated (ignored/used only as hints); NULL means
+ * "no guess" and a deterministic stride sample of the row is used instead
+ * (SPEC.md:287).  prev_topk may equal out_idx (in-place update of the feedback
+ * buffer); any other overlap is an error.  row_lens: nullable device int32
+ * [num_rows] (NULL => every row has row_stride elements). */
+gvr_status gvr_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                            int32_t num_rows, const int32_t* prev_topk, int32_t k,
+                            int32_t* out_idx, cudaStream_t stream);
+
+/* Same as gvr_topk_batched plus: opt (nullable), out_val (nullable device fp32
+ * [num_rows, k]: the selected scores x[out_idx], 0 for padding),
+ * stats (nullable device gvr_row_stats [num_rows]). */
+gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                               int32_t num_rows, const int32_t* prev_topk, int32_t k,
+                               int32_t* out_idx, cudaStream_t stream, const gvr_options* opt,
+                               float* out_val, gvr_row_stats* stats);
+
+/* Radix-select baseline: 2048-bin shared-memory histogram rounds
+ * over the sortable key (11/11/10 bits) with global re-reads and an early exit to an
+ * in-shared-memory finish once the threshold bucket holds <= 2048 elements.  Same
+ * output contract as gvr_topk_batched. */
+gvr_status radix_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                              int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream);
+
+gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                                 int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                                 float* out_val, gvr_row_stats* stats);
+
+/* ---- host-buffer entry point (end-to-end use) ------------------------------------
+ * A workspace owns device buffers for up to max_rows rows of row_stride elements and
+ * k outputs.  gvr_topk_batched_host copies HOST scores/row_lens/prev (pinned memory
+ * recommended) to the device on `stream`, runs gvr_topk_batched, copies the result
+ * into HOST out_idx and synchronises `stream` before returning.  h_row_lens and
+ * h_prev are nullable.  Returns GVR_ERR_INVALID_ARGUMENT if num_rows > max_rows or
+ * the stride/k differ from the workspace's. */
+typedef struct gvr_workspace gvr_workspace;
+gvr_status gvr_workspace_create(int32_t max_rows, int64_t row_stride, int32_t k,
+                                gvr_workspace** ws);
+gvr_status gvr_workspace_destroy(gvr_workspace* ws);
+gvr_status gvr_topk_batched_host(const float* h_scores, int64_t row_stride,
+                                 const int32_t* h_row_lens, int32_t num_rows,
+                                 const int32_t* h_prev, int32_t k, int32_t* h_out,
+                                 gvr_workspace* ws, cudaStream_t stream);
+
+/* Static string for a status code (never NULL). */
+const char* gvr_status_string(gvr_status s);
+
+/* Library/ABI version: major*10000 + minor*100 + patch. */
+int32_t gvr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVR_TOPK_H */

@@ -1,0 +1,205 @@
+"""paper_2604_22312_b200 — B200-native GVR exact Top-K (arXiv 2604.22312).
+
+Thin ctypes binding over the C ABI of ``libgvrtopk.so`` (declared in
+``include/gvr_topk.h``).  This module only marshals arguments: every step of the
+Top-K path runs in the CUDA kernels of the shared library.  There is no CPU or
+PyTorch fallback — if the library or a CUDA device is missing, calls raise.
+
+    topk(scores, k=2048, row_lens=None, prev=None)   -> int32 [R, k] (GVR)
+    radix_topk(scores, k=2048, row_lens=None)         -> int32 [R, k] (radix baseline)
+    topk_ex(...)                                      -> (idx, values, stats)
+    topk_host(scores_np, ...)                         -> host-buffer C-ABI entry point
+
+``scores`` is a CUDA fp32 tensor [R, S] whose last dim is contiguous (any row
+stride); ``row_lens`` an int32 CUDA tensor [R] or None; ``prev`` an int32 CUDA tensor
+[R, k] (the previous decode step's Top-K) or None.  Output order: score descending,
+index ascending; rows shorter than k are padded with -1.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgvrtopk.so")
+_lib = None
+
+STATS_FIELDS = ("secant_iters", "snap_iters", "cand_count", "done_kind", "global_passes",
+                "raises", "buffer_count", "cluster")
+DONE_KINDS = {0: "trivial", 1: "converged", 2: "tiefill", 3: "radix"}
+MAX_K = 2048
+
+
+class GvrOptions(ctypes.Structure):
+    _fields_ = [("collect_sigma", ctypes.c_float), ("max_secant_iters", ctypes.c_int32),
+                ("force_cluster", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class GvrError(RuntimeError):
+    pass
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise GvrError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    sigs = {
+        "gvr_topk_batched": [vp, i64, vp, i32, vp, i32, vp, vp],
+        "gvr_topk_batched_ex": [vp, i64, vp, i32, vp, i32, vp, vp, vp, vp, vp],
+        "radix_topk_batched": [vp, i64, vp, i32, i32, vp, vp],
+        "radix_topk_batched_ex": [vp, i64, vp, i32, i32, vp, vp, vp, vp],
+        "gvr_workspace_create": [i32, i64, i32, ctypes.POINTER(vp)],
+        "gvr_workspace_destroy": [vp],
+        "gvr_topk_batched_host": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
+    }
+    for name, args in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.gvr_status_string.argtypes = [ctypes.c_int]
+    lib.gvr_status_string.restype = ctypes.c_char_p
+    lib.gvr_version.argtypes = []
+    lib.gvr_version.restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+def library():
+    """The loaded ctypes library (loads it on first use)."""
+    return _load()
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise GvrError(_load().gvr_status_string(rc).decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _prep(scores, k, row_lens, prev, out):
+    torch = _torch()
+    if not isinstance(scores, torch.Tensor) or not scores.is_cuda:
+        raise GvrError("scores must be a CUDA tensor (no CPU path)")
+    if scores.dtype != torch.float32 or scores.dim() != 2 or scores.stride(1) != 1:
+        raise GvrError("scores must be fp32 [R, S] with a contiguous last dim")
+    R = scores.shape[0]
+    stride = scores.stride(0) if R > 1 else max(scores.shape[1], 1)
+    if row_lens is not None:
+        if row_lens.dtype != torch.int32 or row_lens.shape != (R,) or not row_lens.is_cuda:
+            raise GvrError("row_lens must be int32 CUDA [R]")
+        row_lens = row_lens.contiguous()
+    elif scores.shape[1] != stride:
+        row_lens = torch.full((R,), scores.shape[1], dtype=torch.int32, device=scores.device)
+    if prev is not None:
+        if prev.dtype != torch.int32 or prev.shape != (R, k) or not prev.is_cuda or not prev.is_contiguous():
+            raise GvrError("prev must be a contiguous int32 CUDA tensor [R, k]")
+    if out is None:
+        out = torch.empty((R, k), dtype=torch.int32, device=scores.device)
+    elif out.dtype != torch.int32 or out.shape != (R, k) or not out.is_contiguous():
+        raise GvrError("out must be a contiguous int32 tensor [R, k]")
+    return R, stride, row_lens, prev, out
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def topk(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None):
+    """GVR exact ordered Top-K of every row (launch is stream-ordered, no host sync)."""
+    R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
+    _check(_load().gvr_topk_batched(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
+                                    _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def topk_ex(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, values: bool = True,
+            stats: bool = True, options: GvrOptions | None = None, stream=None):
+    """GVR Top-K plus optional selected values [R, k] and per-row stats [R, 8] (int32)."""
+    torch = _torch()
+    R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
+    val = torch.empty((R, k), dtype=torch.float32, device=scores.device) if values else None
+    st = torch.zeros((R, len(STATS_FIELDS)), dtype=torch.int32, device=scores.device) if stats else None
+    opt = ctypes.byref(options) if options is not None else None
+    _check(_load().gvr_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
+                                       _ptr(out), _stream_ptr(stream), opt, _ptr(val), _ptr(st)))
+    return out, val, st
+
+
+def radix_topk(scores, k: int = MAX_K, row_lens=None, out=None, stream=None):
+    """Radix-select baseline with the same output contract."""
+    R, stride, row_lens, _, out = _prep(scores, k, row_lens, None, out)
+    _check(_load().radix_topk_batched(_ptr(scores), stride, _ptr(row_lens), R, k, _ptr(out),
+                                      _stream_ptr(stream)))
+    return out
+
+
+def radix_topk_ex(scores, k: int = MAX_K, row_lens=None, out=None, values=True, stats=True, stream=None):
+    torch = _torch()
+    R, stride, row_lens, _, out = _prep(scores, k, row_lens, None, out)
+    val = torch.empty((R, k), dtype=torch.float32, device=scores.device) if values else None
+    st = torch.zeros((R, len(STATS_FIELDS)), dtype=torch.int32, device=scores.device) if stats else None
+    _check(_load().radix_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, k, _ptr(out),
+                                         _stream_ptr(stream), _ptr(val), _ptr(st)))
+    return out, val, st
+
+
+class Workspace:
+    """Device buffers for the host-buffer entry point (gvr_topk_batched_host)."""
+
+    def __init__(self, max_rows: int, row_stride: int, k: int = MAX_K):
+        h = ctypes.c_void_p()
+        _check(_load().gvr_workspace_create(max_rows, row_stride, k, ctypes.byref(h)))
+        self._h, self.max_rows, self.row_stride, self.k = h, max_rows, row_stride, k
+
+    def close(self):
+        if self._h:
+            _load().gvr_workspace_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def topk_host(scores: np.ndarray, ws: Workspace, k: int = MAX_K, row_lens: np.ndarray | None = None,
+              prev: np.ndarray | None = None, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+    """End-to-end entry: HOST fp32 scores [R, stride] (pinned recommended) -> HOST int32
+    [R, k].  H2D copies, the GVR kernel and the D2H copy run inside the C call."""
+    if scores.dtype != np.float32 or scores.ndim != 2 or not scores.flags.c_contiguous:
+        raise GvrError("scores must be a C-contiguous fp32 [R, stride] array")
+    R, stride = scores.shape
+    if out is None:
+        out = np.empty((R, k), dtype=np.int32)
+    lp = None if row_lens is None else ctypes.c_void_p(row_lens.ctypes.data)
+    pp = None if prev is None else ctypes.c_void_p(prev.ctypes.data)
+    sp = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
+    _check(_load().gvr_topk_batched_host(ctypes.c_void_p(scores.ctypes.data), stride, lp, R, pp, k,
+                                         ctypes.c_void_p(out.ctypes.data), ws._h, sp))
+    return out
+
+
+def topk_host_ptr(scores_ptr: int, stride: int, R: int, ws: Workspace, k: int, out_ptr: int,
+                  prev_ptr: int | None = None, lens_ptr: int | None = None, stream=None):
+    """Same as topk_host on raw (pinned) host pointers."""
+    sp = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)
+    _check(_load().gvr_topk_batched_host(ctypes.c_void_p(scores_ptr), stride,
+                                         None if lens_ptr is None else ctypes.c_void_p(lens_ptr), R,
+                                         None if prev_ptr is None else ctypes.c_void_p(prev_ptr), k,
+                                         ctypes.c_void_p(out_ptr), ws._h, sp))

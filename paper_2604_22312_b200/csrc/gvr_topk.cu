@@ -1,0 +1,191 @@
+// gvr_topk.cu — C ABI of libgvrtopk.so (declared in include/gvr_topk.h): argument
+// validation, launch configuration and the host-buffer workspace entry point.
+#include <type_traits>
+
+#include "../../include/gvr_topk.h"
+#include "gvr_kernel.cuh"
+#include "radix_kernel.cuh"
+
+namespace {
+
+using namespace gvr;
+
+constexpr int kVersion = 1 * 10000 + 0 * 100 + 0;
+
+bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb)
+{
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return pa < pb + nb && pb < pa + na;
+}
+
+gvr_status validate(const float* scores, int64_t row_stride, int32_t num_rows, int32_t k, const int32_t* out)
+{
+    if (num_rows < 0 || k < 1 || row_stride < 1) return GVR_ERR_INVALID_ARGUMENT;
+    if (k > GVR_MAX_K) return GVR_ERR_UNSUPPORTED;
+    if (row_stride > 0x7fffffffLL) return GVR_ERR_UNSUPPORTED;
+    if (num_rows > 0 && (scores == nullptr || out == nullptr)) return GVR_ERR_INVALID_ARGUMENT;
+    return GVR_OK;
+}
+
+template <class Kern>
+gvr_status set_smem(Kern kern)
+{
+    // Opt in to > 48 KB dynamic shared memory; idempotent and cheap.
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    return GVR_OK;
+}
+
+gvr_status launch_status()
+{
+    return cudaGetLastError() == cudaSuccess ? GVR_OK : GVR_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gvr_status_string(gvr_status s)
+{
+    switch (s) {
+    case GVR_OK: return "GVR_OK";
+    case GVR_ERR_INVALID_ARGUMENT: return "GVR_ERR_INVALID_ARGUMENT";
+    case GVR_ERR_UNSUPPORTED: return "GVR_ERR_UNSUPPORTED";
+    case GVR_ERR_CUDA: return "GVR_ERR_CUDA";
+    default: return "GVR_ERR_UNKNOWN";
+    }
+}
+
+int32_t gvr_version(void) { return kVersion; }
+
+gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                               const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                               const gvr_options* opt, float* out_val, gvr_row_stats* stats)
+{
+    gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
+    if (st != GVR_OK) return st;
+    if (num_rows == 0) return GVR_OK;
+    const size_t bytes = (size_t)num_rows * (size_t)k * sizeof(int32_t);
+    if (prev_topk && prev_topk != out_idx && ranges_overlap(prev_topk, bytes, out_idx, bytes))
+        return GVR_ERR_INVALID_ARGUMENT;
+    GvrParams prm;
+    prm.collect_sigma = 0.5f;
+    prm.max_secant = 8;
+    if (opt) {
+        if (opt->collect_sigma == opt->collect_sigma) prm.collect_sigma = opt->collect_sigma;
+        if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
+    }
+    if ((st = set_smem(gvr_topk_kernel)) != GVR_OK) return st;
+    gvr_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, prev_topk, k, out_idx,
+                                                          out_val, stats, prm);
+    return launch_status();
+}
+
+gvr_status gvr_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                            const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream)
+{
+    return gvr_topk_batched_ex(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, nullptr,
+                               nullptr, nullptr);
+}
+
+gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                                 int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                                 float* out_val, gvr_row_stats* stats)
+{
+    gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
+    if (st != GVR_OK) return st;
+    if (num_rows == 0) return GVR_OK;
+    if ((st = set_smem(radix_topk_kernel)) != GVR_OK) return st;
+    radix_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
+                                                            stats);
+    return launch_status();
+}
+
+gvr_status radix_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                              int32_t k, int32_t* out_idx, cudaStream_t stream)
+{
+    return radix_topk_batched_ex(scores, row_stride, row_lens, num_rows, k, out_idx, stream, nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------ host-buffer path
+struct gvr_workspace {
+    int32_t max_rows;
+    int64_t row_stride;
+    int32_t k;
+    float* d_scores;
+    int32_t* d_lens;
+    int32_t* d_prev;
+    int32_t* d_out;
+};
+
+gvr_status gvr_workspace_create(int32_t max_rows, int64_t row_stride, int32_t k, gvr_workspace** ws)
+{
+    if (!ws || max_rows < 1 || row_stride < 1 || k < 1) return GVR_ERR_INVALID_ARGUMENT;
+    if (k > GVR_MAX_K || row_stride > 0x7fffffffLL) return GVR_ERR_UNSUPPORTED;
+    *ws = nullptr;
+    gvr_workspace* w = new (std::nothrow) gvr_workspace();
+    if (!w) return GVR_ERR_CUDA;
+    w->max_rows = max_rows;
+    w->row_stride = row_stride;
+    w->k = k;
+    const size_t ns = (size_t)max_rows * (size_t)row_stride * sizeof(float);
+    const size_t no = (size_t)max_rows * (size_t)k * sizeof(int32_t);
+    bool ok = cudaMalloc(&w->d_scores, ns) == cudaSuccess;
+    ok = ok && cudaMalloc(&w->d_lens, (size_t)max_rows * sizeof(int32_t)) == cudaSuccess;
+    ok = ok && cudaMalloc(&w->d_prev, no) == cudaSuccess;
+    ok = ok && cudaMalloc(&w->d_out, no) == cudaSuccess;
+    if (!ok) {
+        (void)cudaGetLastError();
+        gvr_workspace_destroy(w);
+        return GVR_ERR_CUDA;
+    }
+    *ws = w;
+    return GVR_OK;
+}
+
+gvr_status gvr_workspace_destroy(gvr_workspace* ws)
+{
+    if (!ws) return GVR_OK;
+    cudaFree(ws->d_scores);
+    cudaFree(ws->d_lens);
+    cudaFree(ws->d_prev);
+    cudaFree(ws->d_out);
+    delete ws;
+    return GVR_OK;
+}
+
+gvr_status gvr_topk_batched_host(const float* h_scores, int64_t row_stride, const int32_t* h_row_lens,
+                                 int32_t num_rows, const int32_t* h_prev, int32_t k, int32_t* h_out,
+                                 gvr_workspace* ws, cudaStream_t stream)
+{
+    if (!ws) return GVR_ERR_INVALID_ARGUMENT;
+    gvr_status st = validate(h_scores, row_stride, num_rows, k, h_out);
+    if (st != GVR_OK) return st;
+    if (num_rows > ws->max_rows || row_stride != ws->row_stride || k != ws->k) return GVR_ERR_INVALID_ARGUMENT;
+    if (num_rows == 0) return GVR_OK;
+    const size_t ns = (size_t)num_rows * (size_t)row_stride * sizeof(float);
+    const size_t no = (size_t)num_rows * (size_t)k * sizeof(int32_t);
+    bool ok = cudaMemcpyAsync(ws->d_scores, h_scores, ns, cudaMemcpyHostToDevice, stream) == cudaSuccess;
+    if (ok && h_row_lens)
+        ok = cudaMemcpyAsync(ws->d_lens, h_row_lens, (size_t)num_rows * sizeof(int32_t), cudaMemcpyHostToDevice,
+                             stream) == cudaSuccess;
+    if (ok && h_prev) ok = cudaMemcpyAsync(ws->d_prev, h_prev, no, cudaMemcpyHostToDevice, stream) == cudaSuccess;
+    if (!ok) {
+        (void)cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    st = gvr_topk_batched(ws->d_scores, row_stride, h_row_lens ? ws->d_lens : nullptr, num_rows,
+                          h_prev ? ws->d_prev : nullptr, k, ws->d_out, stream);
+    if (st != GVR_OK) return st;
+    if (cudaMemcpyAsync(h_out, ws->d_out, no, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    return GVR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// radix_kernel.cuh — in-house radix-select baseline (Sec. 2.2).
+//
+// One CTA (512 threads) per row, the same thread geometry as the GVR kernel (the
+// paper's "identical thread-level resources").  Each round is a
+// full-row histogram pass over global memory into a 2048-bin shared-memory histogram
+// with atomicAdd, a K-th-bin search over the bin totals (the
+// prefix-sum / find-threshold steps), and a narrowing of the key
+// prefix.  Digits are key bits [31:21], [20:10], [9:0] (the 11/11/10 schedule of
+// PAPER.md:138; R18).  As soon as the threshold bucket holds <= 2048
+// elements the round loop exits early and one filter pass collects
+// every element at or above the bucket into shared memory, where the exact ordered
+// result is finished.  With all 32 bits resolved the K-th key is exact and ties are
+// filled in index order.  Same ordered-output stage as GVR.
+#pragma once
+#include "select_global.cuh"
+
+namespace gvr {
+
+__global__ void __launch_bounds__(NT, 2)
+radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
+                  int32_t* __restrict__ out, float* out_val, gvr_row_stats* stats)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Ctx c = make_ctx(smem_raw);
+    const int r = blockIdx.x;
+    int n = (int)stride;
+    if (row_lens) n = min(max(row_lens[r], 0), (int)stride);
+    const float* x = scores + (int64_t)r * stride;
+    int32_t* o = out + (int64_t)r * k;
+    float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
+    const RowGeom g = make_geom(x, n);
+    int passes = 0, cand = 0, done = GVR_DONE_RADIX;
+
+    if (n <= k) {
+        small_row_emit(c, g, k, o, ov);
+        passes = 1;
+        cand = n;
+        done = GVR_DONE_TRIVIAL;
+    } else {
+        const RadixResult rr = radix_select_global(c, g, (uint32_t)k, true);
+        passes = rr.rounds + 1;
+        if (!rr.exact) {
+            // early exit: everything >= the bucket's lower bound fits (< K + 2048)
+            int fill = 0;
+            const uint32_t lb = rr.prefix;
+            for_each_tile(g, c.tid, [&](auto& tl, int) {
+                commit_unordered(c, tl, [&](uint32_t kk) { return kk >= lb; }, fill);
+                return 0;
+            });
+            __syncthreads();
+            cand = fill;
+            sort_and_emit(c, fill, k, k, o, ov);
+        } else {
+            cand = (int)(rr.above + rr.bucket);
+            if (rr.above + rr.bucket <= (uint32_t)SORT_MAX) {
+                int fill = 0;
+                const uint32_t T = rr.prefix;
+                for_each_tile(g, c.tid, [&](auto& tl, int) {
+                    commit_unordered(c, tl, [&](uint32_t kk) { return kk >= T; }, fill);
+                    return 0;
+                });
+                __syncthreads();
+                sort_and_emit(c, fill, k, k, o, ov);
+            } else {
+                tiefill_emit(c, g, rr.prefix, rr.above, k, k, o, ov);
+            }
+        }
+    }
+    if (stats && c.tid == 0) {
+        gvr_row_stats s;
+        s.secant_iters = 0;
+        s.snap_iters = 0;
+        s.cand_count = cand;
+        s.done_kind = done;
+        s.global_passes = passes;
+        s.raises = 0;
+        s.buffer_count = 0;
+        s.cluster = 1;
+        stats[r] = s;
+    }
+}
+
+}  // namespace gvr
