@@ -88,61 +88,72 @@ def algorithmic_bytes(lens, k=K):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi samples during the timed region (clock + throttle reasons)."""
+    """SM clock + clock-event (throttle) reasons sampled through NVML in a background
+    thread during the timed region (nvidia-smi's own sampler starts too slowly for a
+    millisecond-scale region); falls back to nothing if NVML is unavailable."""
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, gpu_index, period_s: float = 0.002):
+        self.gpu = int(gpu_index) if str(gpu_index).isdigit() else 0
+        self.period = period_s
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            time.sleep(0.01)
         except Exception:
-            self.proc = None
+            self._nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        p = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)
+                rs = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def sample_now(self):
+        if self._nvml is not None:
+            p = self._nvml
+            try:
+                self.samples.append((p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM),
+                                     p.nvmlDeviceGetCurrentClocksEventReasons(self._h)))
+            except Exception:
+                pass
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._nvml is not None:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 3:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                bits = int(parts[2], 16)
-            except ValueError:
-                continue
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        reasons = set()
+        for _, bits in self.samples:
             for b, name in REASON_BITS.items():
                 if bits & b:
                     reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml"}
 
 
 # ----------------------------------------------------------------------------- timing
-def time_steps(fn, batches, steps, warmup, stream):
+def time_steps(fn, batches, steps, warmup, stream, sampler=None):
     import torch
     for i in range(warmup):
         fn(batches[i % len(batches)])
@@ -152,6 +163,8 @@ def time_steps(fn, batches, steps, warmup, stream):
     for i in range(steps):
         fn(batches[i % len(batches)])
     ev1.record(stream)
+    if sampler is not None:
+        sampler.sample_now()  # GPU still executing the queued steps
     torch.cuda.synchronize()
     return ev0.elapsed_time(ev1) / 1e3  # seconds
 
@@ -245,7 +258,7 @@ def main():
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     phys = vis.split(",")[local_rank] if vis else str(local_rank)
     with ClockSampler(phys) as clk:
-        elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream)
+        elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk)
     if dist is not None:
         t = torch.tensor([elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

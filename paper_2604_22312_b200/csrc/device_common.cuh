@@ -1,7 +1,7 @@
 // device_common.cuh — shared device building blocks of the GVR / radix Top-K kernels
-// (sm_100a).  Block-level reductions and scans over 16 warps, the sortable key
-// transform, the shared-memory candidate buffer layout, the in-place chunked
-// compaction, the K-th-bin search, and the ordered-output block sort.
+// (sm_100a): shared-memory layout, the sortable key transform, block reductions and
+// scans over 16 warps, the candidate-buffer count cache and in-place compaction, the
+// K-th-bin search, and the ordered-output stage.
 //
 // PAPER.md references are to /root/reference/PAPER.md (arXiv 2604.22312).
 #pragma once
@@ -21,53 +21,70 @@ constexpr int KMAX = GVR_MAX_K;         // 2048
 constexpr int CWIN = GVR_WINDOW_C;      // Lemma-1 window upper bound C
 constexpr int CHUNK_SLOTS = 8;          // buffer slots per thread per compaction chunk
 constexpr int CHUNK = NT * CHUNK_SLOTS; // 4096 entries per chunk
-constexpr int NCHUNK = 3;
-constexpr int CAP = CHUNK * NCHUNK;     // 12288: capacity of the streamed candidate buffer B
+constexpr int NCHUNK = 2;
+constexpr int CAP = CHUNK * NCHUNK;     // 8192: capacity of the streamed candidate buffer B
 constexpr int NBINS = 2048;             // Phase-4 / radix histogram bins
-constexpr int VEC = 4;                  // float4 loads per thread per tile
-constexpr int TILE_VEC = NT * VEC;      // float4s per tile (8192 elements)
-constexpr int SORT_MAX = 8192;          // largest ordered-output sort (64-bit composites)
+constexpr int VEC = 4;                  // float4 loads per thread per register tile
+constexpr int TILE_VEC = NT * VEC;      // float4s per register tile (8192 elements)
+constexpr int SORT_MAX = 8192;          // largest bitonic ordered-output sort (64-bit composites)
+constexpr int CSORT_MAX = 4096;         // largest counting-sort ordered output
+constexpr int CSORT_BIN_MAX = 32;       // counting sort: largest bin sorted by insertion
+constexpr int LIST_MAX = 4096;          // Phase 4: largest K-th-bin member list
 constexpr int RADIX_EARLY = 2048;       // radix early exit
 constexpr unsigned FULL = 0xffffffffu;
 
-static_assert(CAP >= CWIN, "buffer must hold the Lemma-1 window");
-static_assert(SORT_MAX * 8 <= CAP * 8, "sort array aliases the buffer");
+// TMA bulk-copy ring: NSTAGE stages of STAGE_FLOATS fp32 (one "ring tile" = 8 per thread).
+constexpr int NSTAGE = 3;
+constexpr int STAGE_FLOATS = NT * 8;           // 4096
+constexpr int STAGE_BYTES = STAGE_FLOATS * 4;  // 16 KB
 
-// Shared-memory layout (dynamic).  B = {bkey, bidx} is the candidate buffer; the
-// 64-bit sort array aliases its first SORT_MAX*8 bytes.
+static_assert(CAP >= CWIN, "buffer must hold the Lemma-1 window");
+static_assert(SORT_MAX * 8 <= CAP * 8, "bitonic sort array aliases the buffer");
+
+// Shared-memory layout (dynamic).  B = {bkey, bidx} is the candidate buffer (the
+// 64-bit bitonic sort array aliases it).  The ring is idle after the streaming pass
+// and then hosts the histograms, the K-th-bin member list and the counting sort.
 constexpr int OFF_BKEY = 0;
 constexpr int OFF_BIDX = OFF_BKEY + CAP * 4;
-constexpr int OFF_HIST = OFF_BIDX + CAP * 4;
-constexpr int OFF_RED = OFF_HIST + NBINS * 4;      // u32 [2][4][NW]
-constexpr int OFF_REDF = OFF_RED + 2 * 4 * NW * 4; // f32 [2][2][NW]
-constexpr int OFF_MISC = OFF_REDF + 2 * 2 * NW * 4;
-constexpr int SMEM_BYTES = OFF_MISC + 32 * 4;      // 107,392 B -> 2 CTAs per SM
+constexpr int OFF_RING = OFF_BIDX + CAP * 4;
+constexpr int OFF_HIST = OFF_RING;                         // int32 [NBINS]       (ring alias)
+constexpr int OFF_AUX = OFF_RING + NBINS * 4;              // int32 [NBINS]       (ring alias)
+constexpr int OFF_CSORT = OFF_RING + 2 * NBINS * 4;        // u64 [CSORT_MAX]     (ring alias)
+constexpr int OFF_LIST = OFF_AUX;                          // u32 [LIST_MAX]      (ring alias)
+constexpr int OFF_BAR = OFF_RING + NSTAGE * STAGE_BYTES;   // u64 [NSTAGE] mbarriers
+constexpr int OFF_RED = OFF_BAR + 64;                      // u32 [2][4][NW]
+constexpr int OFF_REDF = OFF_RED + 2 * 4 * NW * 4;         // f32 [2][2][NW]
+constexpr int OFF_MISC = OFF_REDF + 2 * 2 * NW * 4;        // int32 [32]
+constexpr int SMEM_BYTES = OFF_MISC + 32 * 4;              // 115,648 B -> 2 CTAs per SM
+static_assert(OFF_CSORT + CSORT_MAX * 8 <= OFF_RING + NSTAGE * STAGE_BYTES, "csort fits the ring");
+static_assert(OFF_LIST + LIST_MAX * 4 <= OFF_RING + NSTAGE * STAGE_BYTES, "list fits the ring (used only in Phase 4)");
+static_assert(2 * (SMEM_BYTES + 1024) <= 233472, "two CTAs per SM");
+
+extern __shared__ __align__(128) unsigned char g_smem[];
+
+__device__ __forceinline__ uint32_t* s_bkey() { return reinterpret_cast<uint32_t*>(g_smem + OFF_BKEY); }
+__device__ __forceinline__ int32_t* s_bidx() { return reinterpret_cast<int32_t*>(g_smem + OFF_BIDX); }
+__device__ __forceinline__ unsigned long long* s_comp() { return reinterpret_cast<unsigned long long*>(g_smem + OFF_BKEY); }
+__device__ __forceinline__ int32_t* s_hist() { return reinterpret_cast<int32_t*>(g_smem + OFF_HIST); }
+__device__ __forceinline__ int32_t* s_aux() { return reinterpret_cast<int32_t*>(g_smem + OFF_AUX); }
+__device__ __forceinline__ unsigned long long* s_csort() { return reinterpret_cast<unsigned long long*>(g_smem + OFF_CSORT); }
+__device__ __forceinline__ uint32_t* s_list() { return reinterpret_cast<uint32_t*>(g_smem + OFF_LIST); }
+__device__ __forceinline__ float* s_ring() { return reinterpret_cast<float*>(g_smem + OFF_RING); }
+__device__ __forceinline__ uint32_t* s_red() { return reinterpret_cast<uint32_t*>(g_smem + OFF_RED); }
+__device__ __forceinline__ float* s_redf() { return reinterpret_cast<float*>(g_smem + OFF_REDF); }
+__device__ __forceinline__ int32_t* s_misc() { return reinterpret_cast<int32_t*>(g_smem + OFF_MISC); }
 
 struct Ctx {
     int tid, lane, warp, par;
-    uint32_t* bkey;
-    int32_t* bidx;
-    unsigned long long* comp;
-    int32_t* hist;
-    uint32_t* red;
-    float* redf;
-    int32_t* misc;
 };
 
-__device__ __forceinline__ Ctx make_ctx(unsigned char* smem)
+__device__ __forceinline__ Ctx make_ctx()
 {
     Ctx c;
     c.tid = threadIdx.x;
     c.lane = threadIdx.x & 31;
     c.warp = threadIdx.x >> 5;
     c.par = 0;
-    c.bkey = reinterpret_cast<uint32_t*>(smem + OFF_BKEY);
-    c.bidx = reinterpret_cast<int32_t*>(smem + OFF_BIDX);
-    c.comp = reinterpret_cast<unsigned long long*>(smem + OFF_BKEY);
-    c.hist = reinterpret_cast<int32_t*>(smem + OFF_HIST);
-    c.red = reinterpret_cast<uint32_t*>(smem + OFF_RED);
-    c.redf = reinterpret_cast<float*>(smem + OFF_REDF);
-    c.misc = reinterpret_cast<int32_t*>(smem + OFF_MISC);
     return c;
 }
 
@@ -89,6 +106,14 @@ __device__ __forceinline__ unsigned long long make_comp(uint32_t key, int32_t id
 {
     return ((unsigned long long)key << 32) | (unsigned long long)(~(uint32_t)idx);
 }
+__device__ __forceinline__ int32_t comp_idx(unsigned long long cv) { return (int32_t)(~(uint32_t)(cv & 0xffffffffull)); }
+__device__ __forceinline__ uint32_t comp_key(unsigned long long cv) { return (uint32_t)(cv >> 32); }
+
+// Float-domain superset test of key(x) >= key(tf): !(x < tf) holds for every x whose
+// key is >= key(tf) (key order refines float order; NaN x and NaN tf pass).  Elements
+// that pass spuriously (NaN, -0 against +0) are harmless: every later count and the
+// output use exact key comparisons.
+__device__ __forceinline__ bool pass_ge(float x, float tf) { return !(x < tf); }
 
 // Streaming 128-bit load: read-only path, no L1 allocation, 256B L2 prefetch.
 __device__ __forceinline__ float4 ldg_stream(const float4* p)
@@ -123,7 +148,7 @@ __device__ __forceinline__ void block_red4(Ctx& c, uint32_t& a, uint32_t& b, uin
     b = wred<O1>(b);
     d = wred<O2>(d);
     e = wred<O3>(e);
-    uint32_t* s = c.red + c.par * 4 * NW;
+    uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 0) {
         s[c.warp] = a;
         s[NW + c.warp] = b;
@@ -144,7 +169,7 @@ __device__ __forceinline__ void block_red2(Ctx& c, uint32_t& a, uint32_t& b)
 {
     a = wred<O0>(a);
     b = wred<O1>(b);
-    uint32_t* s = c.red + c.par * 4 * NW;
+    uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 0) {
         s[c.warp] = a;
         s[NW + c.warp] = b;
@@ -160,7 +185,7 @@ template <int O0>
 __device__ __forceinline__ uint32_t block_red1(Ctx& c, uint32_t a)
 {
     a = wred<O0>(a);
-    uint32_t* s = c.red + c.par * 4 * NW;
+    uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 0) s[c.warp] = a;
     __syncthreads();
     a = wred<O0>(c.lane < NW ? s[c.lane] : rident<O0>());
@@ -176,7 +201,7 @@ __device__ __forceinline__ void block_fsum2(Ctx& c, float& a, float& b)
         a += __shfl_xor_sync(FULL, a, o);
         b += __shfl_xor_sync(FULL, b, o);
     }
-    float* s = c.redf + c.par * 2 * NW;
+    float* s = s_redf() + c.par * 2 * NW;
     if (c.lane == 0) {
         s[c.warp] = a;
         s[NW + c.warp] = b;
@@ -203,7 +228,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(Ctx& c, uint32_t v, uint32_t
         uint32_t y = __shfl_up_sync(FULL, x, o);
         if (c.lane >= o) x += y;
     }
-    uint32_t* s = c.red + c.par * 4 * NW;
+    uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 31) s[c.warp] = x;
     __syncthreads();
     const uint32_t w = c.lane < NW ? s[c.lane] : 0u;
@@ -223,6 +248,7 @@ struct ChunkCounts {
 
 __device__ __forceinline__ ChunkCounts count_chunks_ge(const Ctx& c, int fill, uint32_t T)
 {
+    const uint32_t* bkey = s_bkey();
     ChunkCounts cc;
 #pragma unroll
     for (int ch = 0; ch < NCHUNK; ++ch) {
@@ -230,7 +256,7 @@ __device__ __forceinline__ ChunkCounts count_chunks_ge(const Ctx& c, int fill, u
 #pragma unroll
         for (int j = 0; j < CHUNK_SLOTS; ++j) {
             const int p = ch * CHUNK + j * NT + c.tid;
-            if (p < fill && c.bkey[p] >= T) ++n;
+            if (p < fill && bkey[p] >= T) ++n;
         }
         cc.c[ch] = n;
     }
@@ -251,6 +277,8 @@ __device__ __forceinline__ uint32_t chunk_total(const ChunkCounts& cc)
 // the scan barrier, so no slot is overwritten before it is read.  Returns new fill.
 __device__ __forceinline__ int compact_ge(Ctx& c, int fill, uint32_t T, const ChunkCounts& cc)
 {
+    uint32_t* bkey = s_bkey();
+    int32_t* bidx = s_bidx();
     int out_base = 0;
 #pragma unroll
     for (int ch = 0; ch < NCHUNK; ++ch) {
@@ -263,8 +291,8 @@ __device__ __forceinline__ int compact_ge(Ctx& c, int fill, uint32_t T, const Ch
             kk[j] = 0u;
             ii[j] = 0;
             if (p < fill) {
-                kk[j] = c.bkey[p];
-                ii[j] = c.bidx[p];
+                kk[j] = bkey[p];
+                ii[j] = bidx[p];
             }
         }
         uint32_t tot;
@@ -273,8 +301,8 @@ __device__ __forceinline__ int compact_ge(Ctx& c, int fill, uint32_t T, const Ch
         for (int j = 0; j < CHUNK_SLOTS; ++j) {
             const int p = ch * CHUNK + j * NT + c.tid;
             if (p < fill && kk[j] >= T) {
-                c.bkey[pos] = kk[j];
-                c.bidx[pos] = ii[j];
+                bkey[pos] = kk[j];
+                bidx[pos] = ii[j];
                 ++pos;
             }
         }
@@ -284,11 +312,12 @@ __device__ __forceinline__ int compact_ge(Ctx& c, int fill, uint32_t T, const Ch
     return out_base;
 }
 
-// Max key over B[0, fill).
+// Max key over B[0, fill) (thread-local part).
 __device__ __forceinline__ uint32_t buffer_max_local(const Ctx& c, int fill)
 {
+    const uint32_t* bkey = s_bkey();
     uint32_t m = 0;
-    for (int p = c.tid; p < fill; p += NT) m = max(m, c.bkey[p]);
+    for (int p = c.tid; p < fill; p += NT) m = max(m, bkey[p]);
     return m;
 }
 
@@ -299,13 +328,15 @@ __device__ __forceinline__ uint32_t buffer_max_local(const Ctx& c, int fill)
 // owning lane resolves the exact bin.  Requires 1 <= krem <= sum(hist).
 __device__ __forceinline__ void kth_bin(Ctx& c, int nb, uint32_t krem, int& b_out, uint32_t& above_out)
 {
+    const int32_t* hist = s_hist();
+    int32_t* misc = s_misc();
     const int per = nb / NW;  // 128 or 64
     const int q = per / 32;   // 4 or 2
     const int base = c.warp * per + c.lane * q;
     uint32_t ls = 0;
-    for (int i = 0; i < q; ++i) ls += (uint32_t)c.hist[base + i];
+    for (int i = 0; i < q; ++i) ls += (uint32_t)hist[base + i];
     const uint32_t wt = __reduce_add_sync(FULL, ls);
-    uint32_t* s = c.red + c.par * 4 * NW;
+    uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 0) s[c.warp] = wt;
     __syncthreads();
     const uint32_t v = c.lane < NW ? s[c.lane] : 0u;
@@ -320,34 +351,43 @@ __device__ __forceinline__ void kth_bin(Ctx& c, int nb, uint32_t krem, int& b_ou
     if (ls > 0 && above_g < krem && krem <= above_g + ls) {
         uint32_t a = above_g;
         for (int i = q - 1; i >= 0; --i) {
-            const uint32_t h = (uint32_t)c.hist[base + i];
+            const uint32_t h = (uint32_t)hist[base + i];
             if (a + h >= krem) {
-                c.misc[0] = base + i;
-                c.misc[1] = (int32_t)a;
+                misc[0] = base + i;
+                misc[1] = (int32_t)a;
                 break;
             }
             a += h;
         }
     }
     __syncthreads();
-    b_out = c.misc[0];
-    above_out = (uint32_t)c.misc[1];
+    b_out = misc[0];
+    above_out = (uint32_t)misc[1];
     c.par ^= 1;
     __syncthreads();  // misc may be reused immediately
 }
 
-__device__ __forceinline__ void zero_hist(const Ctx& c, int nb)
+__device__ __forceinline__ void zero_hist(const Ctx& c, int32_t* h, int nb)
 {
-    for (int i = c.tid; i < nb; i += NT) c.hist[i] = 0;
+    for (int i = c.tid; i < nb; i += NT) h[i] = 0;
+}
+
+__device__ __forceinline__ int shift_for_width(uint64_t width)
+{
+    int s = 0;
+    while (((width - 1) >> s) >= (uint64_t)NBINS) ++s;
+    return s;
 }
 
 // ---------------------------------------------------------------------------------
-// Ordered output: bitonic sort of P (power of two, <= SORT_MAX) 64-bit composites in
-// shared memory, descending, so that position j holds the j-th element of the
-// (score desc, index asc) order.
+// Ordered output (not part of the paper, whose output is an unordered partition with
+// non-deterministic ties): the selected entries are sorted by
+// the 64-bit composite (key << 32 | ~idx) descending = (score desc, index asc).
+
+// Bitonic fallback: P (power of two, <= SORT_MAX) composites in the aliasing array.
 __device__ __forceinline__ void bitonic_sort_desc(Ctx& c, int P)
 {
-    unsigned long long* a = c.comp;
+    unsigned long long* a = s_comp();
     for (int kk = 2; kk <= P; kk <<= 1) {
         for (int j = kk >> 1; j > 0; j >>= 1) {
             for (int i = c.tid; i < (P >> 1); i += NT) {
@@ -372,40 +412,125 @@ __device__ __forceinline__ int pow2_at_least(int m)
     return p;
 }
 
-// Build composites from B[0, m) into the aliasing sort array, sort, and write the
-// first `take` entries as the row's output (indices, optional values) followed by -1
-// padding up to k.  m <= SORT_MAX.
-__device__ __forceinline__ void sort_and_emit(Ctx& c, int m, int take, int k, int32_t* out,
-                                              float* out_val)
+__device__ __forceinline__ void write_output(const Ctx& c, const unsigned long long* sorted, int take, int k,
+                                             int32_t* out, float* out_val)
 {
-    const int P = pow2_at_least(m);
-    constexpr int PER = SORT_MAX / NT;  // 16
-    unsigned long long v[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const int p = j * NT + c.tid;
-        v[j] = 0ull;
-        if (p < m) v[j] = make_comp(c.bkey[p], c.bidx[p]);
-    }
-    __syncthreads();  // all reads of B done before the aliasing writes
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const int p = j * NT + c.tid;
-        if (p < P) c.comp[p] = v[j];
-    }
-    __syncthreads();
-    bitonic_sort_desc(c, P);
     for (int j = c.tid; j < k; j += NT) {
         int32_t idx = -1;
         float val = 0.f;
         if (j < take) {
-            const unsigned long long cv = c.comp[j];
-            idx = (int32_t)(~(uint32_t)(cv & 0xffffffffull));
-            val = key2f((uint32_t)(cv >> 32));
+            const unsigned long long cv = sorted[j];
+            idx = comp_idx(cv);
+            val = key2f(comp_key(cv));
         }
         out[j] = idx;
         if (out_val) out_val[j] = val;
     }
+}
+
+// Emit the entries of B[0, fill) with key >= Tsel (n_sel of them, n_sel <= SORT_MAX),
+// sorted, as the row's first `take` outputs, then -1 padding up to k.
+// Counting sort: a 2048-bin histogram over [Tsel, kmax] (bin 0 = highest keys), bin
+// offsets by one block scan, scatter with per-bin cursors, then an insertion sort of
+// the (few) entries that share a bin.  Falls back to the bitonic sort when the
+// selection or a bin is too large.
+__device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int n_sel, int take, int k,
+                                            int32_t* out, float* out_val)
+{
+    uint32_t* bkey = s_bkey();
+    int32_t* bidx = s_bidx();
+    uint32_t kmx = 0;
+    for (int p = c.tid; p < fill; p += NT) {
+        const uint32_t kv = bkey[p];
+        if (kv >= Tsel) kmx = max(kmx, kv);
+    }
+    int32_t* hist = s_hist();
+    int32_t* cur = s_aux();
+    zero_hist(c, hist, NBINS);
+    kmx = block_red1<R_MAX>(c, kmx);  // (barrier also orders the zeroing)
+    const int s = shift_for_width((uint64_t)kmx - Tsel + 1ull);
+    bool counting = n_sel <= CSORT_MAX;
+    if (counting) {
+        for (int p = c.tid; p < fill; p += NT) {
+            const uint32_t kv = bkey[p];
+            if (kv >= Tsel) atomicAdd(&hist[(NBINS - 1) - (int)((kv - Tsel) >> s)], 1);
+        }
+        __syncthreads();
+        // exclusive scan over bins (4 consecutive bins per thread)
+        const int b0 = c.tid * 4;
+        int h[4];
+        uint32_t loc = 0, mx = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            h[i] = hist[b0 + i];
+            loc += (uint32_t)h[i];
+            mx = max(mx, (uint32_t)h[i]);
+        }
+        uint32_t tot;
+        uint32_t off = block_excl_scan(c, loc, tot);
+        mx = block_red1<R_MAX>(c, mx);
+        counting = mx <= (uint32_t)CSORT_BIN_MAX;
+        if (counting) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                cur[b0 + i] = (int)off;
+                off += (uint32_t)h[i];
+            }
+            __syncthreads();
+            unsigned long long* cs = s_csort();
+            for (int p = c.tid; p < fill; p += NT) {
+                const uint32_t kv = bkey[p];
+                if (kv >= Tsel) {
+                    const int b = (NBINS - 1) - (int)((kv - Tsel) >> s);
+                    const int slot = atomicAdd(&cur[b], 1);
+                    cs[slot] = make_comp(kv, bidx[p]);
+                }
+            }
+            __syncthreads();
+            // insertion sort inside each bin (cur[b] now = end of bin b)
+            for (int b = c.tid; b < NBINS; b += NT) {
+                const int cnt = hist[b];
+                if (cnt > 1) {
+                    const int st = cur[b] - cnt;
+                    for (int i = st + 1; i < st + cnt; ++i) {
+                        const unsigned long long v = cs[i];
+                        int j = i - 1;
+                        while (j >= st && cs[j] < v) {
+                            cs[j + 1] = cs[j];
+                            --j;
+                        }
+                        cs[j + 1] = v;
+                    }
+                }
+            }
+            __syncthreads();
+            write_output(c, cs, take, k, out, out_val);
+            return;
+        }
+    }
+    // bitonic fallback: gather the selection into the aliasing composite array
+    constexpr int PER = SORT_MAX / NT;  // 16
+    unsigned long long v[PER];
+    // compact the selected entries of this thread's slots first (order-free)
+    ChunkCounts cc = count_chunks_ge(c, fill, Tsel);
+    const int m = compact_ge(c, fill, Tsel, cc);
+    const int P = pow2_at_least(m);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int p = j * NT + c.tid;
+        v[j] = 0ull;
+        if (p < m) v[j] = make_comp(bkey[p], bidx[p]);
+    }
+    __syncthreads();  // all reads of B done before the aliasing writes
+    unsigned long long* comp = s_comp();
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int p = j * NT + c.tid;
+        if (p < P) comp[p] = v[j];
+    }
+    __syncthreads();
+    bitonic_sort_desc(c, P);
+    write_output(c, comp, take, k, out, out_val);
 }
 
 }  // namespace gvr

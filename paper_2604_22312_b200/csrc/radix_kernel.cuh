@@ -20,8 +20,7 @@ __global__ void __launch_bounds__(NT, 2)
 radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   int32_t* __restrict__ out, float* out_val, gvr_row_stats* stats)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Ctx c = make_ctx(smem_raw);
+    Ctx c = make_ctx();
     const int r = blockIdx.x;
     int n = (int)stride;
     if (row_lens) n = min(max(row_lens[r], 0), (int)stride);
@@ -49,7 +48,7 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             });
             __syncthreads();
             cand = fill;
-            sort_and_emit(c, fill, k, k, o, ov);
+            emit_sorted(c, fill, 0u, fill, k, k, o, ov);
         } else {
             cand = (int)(rr.above + rr.bucket);
             if (rr.above + rr.bucket <= (uint32_t)SORT_MAX) {
@@ -60,7 +59,7 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                     return 0;
                 });
                 __syncthreads();
-                sort_and_emit(c, fill, k, k, o, ov);
+                emit_sorted(c, fill, 0u, fill, k, k, o, ov);
             } else {
                 tiefill_emit(c, g, rr.prefix, rr.above, k, k, o, ov);
             }

@@ -5,6 +5,7 @@
 // the GVR fallback for massive ties.
 #pragma once
 #include "row_tiles.cuh"
+#include "pipeline.cuh"
 
 namespace gvr {
 
@@ -13,6 +14,8 @@ namespace gvr {
 template <class Tile, class Pred>
 __device__ __forceinline__ void commit_unordered(Ctx& c, const Tile& tl, Pred pred, int& fill)
 {
+    uint32_t* bkey = s_bkey();
+    int32_t* bidx = s_bidx();
     uint32_t cnt = 0;
 #pragma unroll
     for (int e = 0; e < Tile::E; ++e)
@@ -22,8 +25,8 @@ __device__ __forceinline__ void commit_unordered(Ctx& c, const Tile& tl, Pred pr
 #pragma unroll
     for (int e = 0; e < Tile::E; ++e) {
         if (tl.valid(e) && pred(tl.key[e])) {
-            c.bkey[pos] = tl.key[e];
-            c.bidx[pos] = tl.idx(e);
+            bkey[pos] = tl.key[e];
+            bidx[pos] = tl.idx(e);
             ++pos;
         }
     }
@@ -55,13 +58,14 @@ __device__ __forceinline__ RadixResult radix_select_global(Ctx& c, const RowGeom
         const int bits = round == 2 ? 10 : 11;
         const uint32_t dmask = (1u << bits) - 1u;
         const int nb = 1 << bits;
-        zero_hist(c, nb);
+        int32_t* hist = s_hist();
+        zero_hist(c, hist, nb);
         __syncthreads();
         for_each_tile(g, c.tid, [&](auto& tl, int) {
 #pragma unroll
             for (int e = 0; e < tl.E; ++e) {
                 const uint32_t k = tl.key[e];
-                if (tl.valid(e) && (k & pmask) == prefix) atomicAdd(&c.hist[(k >> shift) & dmask], 1);
+                if (tl.valid(e) && (k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & dmask], 1);
             }
             return 0;
         });
@@ -69,7 +73,7 @@ __device__ __forceinline__ RadixResult radix_select_global(Ctx& c, const RowGeom
         int b;
         uint32_t a;
         kth_bin(c, nb, krem, b, a);
-        const uint32_t cb = (uint32_t)c.hist[b];
+        const uint32_t cb = (uint32_t)hist[b];
         above += a;
         krem -= a;
         prefix |= (uint32_t)b << shift;
@@ -95,6 +99,8 @@ __device__ __forceinline__ RadixResult radix_select_global(Ctx& c, const RowGeom
 __device__ __forceinline__ void tiefill_emit(Ctx& c, const RowGeom& g, uint32_t Tstar, uint32_t n_gt,
                                              int K, int k, int32_t* out, float* out_val)
 {
+    uint32_t* bkey = s_bkey();
+    int32_t* bidx = s_bidx();
     const uint32_t need = (uint32_t)K - n_gt;
     int fill_gt = 0;
     uint32_t ties = 0;
@@ -105,7 +111,7 @@ __device__ __forceinline__ void tiefill_emit(Ctx& c, const RowGeom& g, uint32_t 
         if (ties < need) {
             // ties, ranked in index order: for a MainTile the four lanes of float4 slot j
             // of all threads form one index-ordered column
-            constexpr int COLS = (sizeof(tl.key) / sizeof(uint32_t) + 3) / 4;
+            constexpr int COLS = (std::remove_reference_t<decltype(tl)>::E + 3) / 4;
 #pragma unroll
             for (int j = 0; j < COLS; ++j) {
                 uint32_t cnt = 0;
@@ -121,8 +127,8 @@ __device__ __forceinline__ void tiefill_emit(Ctx& c, const RowGeom& g, uint32_t 
                     const int e = 4 * j + q;
                     if (e < tl.E && tl.valid(e) && tl.key[e] == Tstar) {
                         if (r < need) {
-                            c.bkey[tie_base + r] = Tstar;
-                            c.bidx[tie_base + r] = tl.idx(e);
+                            bkey[tie_base + r] = Tstar;
+                            bidx[tie_base + r] = tl.idx(e);
                         }
                         ++r;
                     }
@@ -135,11 +141,11 @@ __device__ __forceinline__ void tiefill_emit(Ctx& c, const RowGeom& g, uint32_t 
     __syncthreads();
     // move the ties behind the > Tstar entries
     for (int i = c.tid; i < (int)need; i += NT) {
-        c.bkey[n_gt + i] = c.bkey[tie_base + i];
-        c.bidx[n_gt + i] = c.bidx[tie_base + i];
+        bkey[n_gt + i] = bkey[tie_base + i];
+        bidx[n_gt + i] = bidx[tie_base + i];
     }
     __syncthreads();
-    sort_and_emit(c, K, K, k, out, out_val);
+    emit_sorted(c, K, 0u, K, K, k, out, out_val);
 }
 
 // Rows with len <= k: every element, sorted, then -1 padding (R5).
@@ -151,7 +157,7 @@ __device__ __forceinline__ void small_row_emit(Ctx& c, const RowGeom& g, int k, 
         return 0;
     });
     __syncthreads();
-    sort_and_emit(c, g.n, g.n, k, out, out_val);
+    emit_sorted(c, g.n, 0u, g.n, g.n, k, out, out_val);
 }
 
 }  // namespace gvr
