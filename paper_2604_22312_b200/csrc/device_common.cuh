@@ -15,50 +15,56 @@ namespace gvr {
 
 // ---------------------------------------------------------------------------------
 // Geometry and capacities.
-constexpr int NT = 512;                 // threads per CTA
-constexpr int NW = NT / 32;             // 16 warps
+constexpr int NT = 256;                 // threads per CTA (the paper uses 512)
+constexpr int NW = NT / 32;             // 8 warps (the paper's K-th-bin search uses 16)
 constexpr int KMAX = GVR_MAX_K;         // 2048
 constexpr int CWIN = GVR_WINDOW_C;      // Lemma-1 window upper bound C
 constexpr int CHUNK_SLOTS = 8;          // buffer slots per thread per compaction chunk
-constexpr int CHUNK = NT * CHUNK_SLOTS; // 4096 entries per chunk
-constexpr int NCHUNK = 2;
+constexpr int CHUNK = NT * CHUNK_SLOTS; // 2048 entries per chunk
+constexpr int NCHUNK = 4;
 constexpr int CAP = CHUNK * NCHUNK;     // 8192: capacity of the streamed candidate buffer B
 constexpr int NBINS = 2048;             // Phase-4 / radix histogram bins
 constexpr int VEC = 4;                  // float4 loads per thread per register tile
 constexpr int TILE_VEC = NT * VEC;      // float4s per register tile (8192 elements)
-constexpr int SORT_MAX = 8192;          // largest bitonic ordered-output sort (64-bit composites)
+constexpr int SORT_MAX = 4096;          // largest bitonic ordered-output sort (64-bit composites)
 constexpr int CSORT_MAX = 4096;         // largest counting-sort ordered output
 constexpr int CSORT_BIN_MAX = 32;       // counting sort: largest bin sorted by insertion
 constexpr int LIST_MAX = 4096;          // Phase 4: largest K-th-bin member list
 constexpr int RADIX_EARLY = 2048;       // radix early exit
 constexpr unsigned FULL = 0xffffffffu;
 
-// TMA bulk-copy ring: NSTAGE stages of STAGE_FLOATS fp32 (one "ring tile" = 8 per thread).
+// TMA bulk-copy ring: NSTAGE stages of STAGE_FLOATS fp32 (16 per thread).
 constexpr int NSTAGE = 3;
-constexpr int STAGE_FLOATS = NT * 8;           // 4096
+constexpr int STAGE_FLOATS = NT * 16;          // 4096
 constexpr int STAGE_BYTES = STAGE_FLOATS * 4;  // 16 KB
 
 static_assert(CAP >= CWIN, "buffer must hold the Lemma-1 window");
-static_assert(SORT_MAX * 8 <= CAP * 8, "bitonic sort array aliases the buffer");
+static_assert(NBINS % NT == 0 && NBINS / NW % 32 == 0, "bin partitioning");
+static_assert(SORT_MAX <= CAP, "bitonic sort array aliases the buffer");
 
-// Shared-memory layout (dynamic).  B = {bkey, bidx} is the candidate buffer (the
-// 64-bit bitonic sort array aliases it).  The ring is idle after the streaming pass
-// and then hosts the histograms, the K-th-bin member list and the counting sort.
+// Shared-memory layout (dynamic): B = {bkey, bidx} is the candidate buffer (the 64-bit
+// bitonic sort array aliases it).  The TMA ring is idle once a row has been streamed
+// and then hosts the work area: histograms, the K-th-bin member list, counting sort.
 constexpr int OFF_BKEY = 0;
 constexpr int OFF_BIDX = OFF_BKEY + CAP * 4;
-constexpr int OFF_RING = OFF_BIDX + CAP * 4;
-constexpr int OFF_HIST = OFF_RING;                         // int32 [NBINS]       (ring alias)
-constexpr int OFF_AUX = OFF_RING + NBINS * 4;              // int32 [NBINS]       (ring alias)
-constexpr int OFF_CSORT = OFF_RING + 2 * NBINS * 4;        // u64 [CSORT_MAX]     (ring alias)
-constexpr int OFF_LIST = OFF_AUX;                          // u32 [LIST_MAX]      (ring alias)
+constexpr int OFF_RING = OFF_BIDX + CAP * 4;               // 64 KB, 128-B aligned
+constexpr int OFF_WORK = OFF_RING;
+constexpr int OFF_HIST = OFF_WORK;                         // int32 [NBINS]     (ring alias)
+constexpr int OFF_AUX = OFF_WORK + NBINS * 4;              // int32 [NBINS]     (ring alias)
+constexpr int OFF_CSORT = OFF_WORK + 2 * NBINS * 4;        // u64 [CSORT_MAX]   (ring alias)
+constexpr int OFF_LIST = OFF_AUX;                          // u32 [LIST_MAX]    (Phase 4 only)
+constexpr int WORK_BYTES = 2 * NBINS * 4 + CSORT_MAX * 8;  // 48 KB
 constexpr int OFF_BAR = OFF_RING + NSTAGE * STAGE_BYTES;   // u64 [NSTAGE] mbarriers
 constexpr int OFF_RED = OFF_BAR + 64;                      // u32 [2][4][NW]
 constexpr int OFF_REDF = OFF_RED + 2 * 4 * NW * 4;         // f32 [2][2][NW]
 constexpr int OFF_MISC = OFF_REDF + 2 * 2 * NW * 4;        // int32 [32]
-constexpr int SMEM_BYTES = OFF_MISC + 32 * 4;              // 115,648 B -> 2 CTAs per SM
-static_assert(OFF_CSORT + CSORT_MAX * 8 <= OFF_RING + NSTAGE * STAGE_BYTES, "csort fits the ring");
-static_assert(OFF_LIST + LIST_MAX * 4 <= OFF_RING + NSTAGE * STAGE_BYTES, "list fits the ring (used only in Phase 4)");
+constexpr int SMEM_BYTES = OFF_MISC + 32 * 4;              // 115,264 B -> 2 CTAs per SM
+static_assert(WORK_BYTES <= NSTAGE * STAGE_BYTES, "work area fits the idle ring");
+static_assert(OFF_LIST + LIST_MAX * 4 <= OFF_WORK + WORK_BYTES, "list fits the work area");
 static_assert(2 * (SMEM_BYTES + 1024) <= 233472, "two CTAs per SM");
+
+// Named barrier 1 over the CTA's NT threads.
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
 extern __shared__ __align__(128) unsigned char g_smem[];
 
@@ -126,7 +132,7 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p)
 }
 
 // ---------------------------------------------------------------------------------
-// Block reductions.  Every call costs one __syncthreads(); scratch slots alternate
+// Block reductions.  Every call costs one csync(); scratch slots alternate
 // (c.par) so back-to-back calls need no second barrier.
 enum { R_ADD = 0, R_MIN = 1, R_MAX = 2 };
 
@@ -155,7 +161,7 @@ __device__ __forceinline__ void block_red4(Ctx& c, uint32_t& a, uint32_t& b, uin
         s[2 * NW + c.warp] = d;
         s[3 * NW + c.warp] = e;
     }
-    __syncthreads();
+    csync();
     const bool in = c.lane < NW;
     a = wred<O0>(in ? s[c.lane] : rident<O0>());
     b = wred<O1>(in ? s[NW + c.lane] : rident<O1>());
@@ -174,7 +180,7 @@ __device__ __forceinline__ void block_red2(Ctx& c, uint32_t& a, uint32_t& b)
         s[c.warp] = a;
         s[NW + c.warp] = b;
     }
-    __syncthreads();
+    csync();
     const bool in = c.lane < NW;
     a = wred<O0>(in ? s[c.lane] : rident<O0>());
     b = wred<O1>(in ? s[NW + c.lane] : rident<O1>());
@@ -187,7 +193,7 @@ __device__ __forceinline__ uint32_t block_red1(Ctx& c, uint32_t a)
     a = wred<O0>(a);
     uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 0) s[c.warp] = a;
-    __syncthreads();
+    csync();
     a = wred<O0>(c.lane < NW ? s[c.lane] : rident<O0>());
     c.par ^= 1;
     return a;
@@ -206,7 +212,7 @@ __device__ __forceinline__ void block_fsum2(Ctx& c, float& a, float& b)
         s[c.warp] = a;
         s[NW + c.warp] = b;
     }
-    __syncthreads();
+    csync();
     a = c.lane < NW ? s[c.lane] : 0.f;
     b = c.lane < NW ? s[NW + c.lane] : 0.f;
 #pragma unroll
@@ -230,7 +236,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(Ctx& c, uint32_t v, uint32_t
     }
     uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 31) s[c.warp] = x;
-    __syncthreads();
+    csync();
     const uint32_t w = c.lane < NW ? s[c.lane] : 0u;
     const uint32_t before = __reduce_add_sync(FULL, c.lane < c.warp ? w : 0u);
     total = __reduce_add_sync(FULL, w);
@@ -308,7 +314,7 @@ __device__ __forceinline__ int compact_ge(Ctx& c, int fill, uint32_t T, const Ch
         }
         out_base += (int)tot;
     }
-    __syncthreads();
+    csync();
     return out_base;
 }
 
@@ -338,7 +344,7 @@ __device__ __forceinline__ void kth_bin(Ctx& c, int nb, uint32_t krem, int& b_ou
     const uint32_t wt = __reduce_add_sync(FULL, ls);
     uint32_t* s = s_red() + c.par * 4 * NW;
     if (c.lane == 0) s[c.warp] = wt;
-    __syncthreads();
+    csync();
     const uint32_t v = c.lane < NW ? s[c.lane] : 0u;
     const uint32_t above_w = __reduce_add_sync(FULL, (c.lane > c.warp && c.lane < NW) ? v : 0u);
     uint32_t x = ls;  // inclusive suffix over lanes
@@ -360,11 +366,11 @@ __device__ __forceinline__ void kth_bin(Ctx& c, int nb, uint32_t krem, int& b_ou
             a += h;
         }
     }
-    __syncthreads();
+    csync();
     b_out = misc[0];
     above_out = (uint32_t)misc[1];
     c.par ^= 1;
-    __syncthreads();  // misc may be reused immediately
+    csync();  // misc may be reused immediately
 }
 
 __device__ __forceinline__ void zero_hist(const Ctx& c, int32_t* h, int nb)
@@ -372,11 +378,12 @@ __device__ __forceinline__ void zero_hist(const Ctx& c, int32_t* h, int nb)
     for (int i = c.tid; i < nb; i += NT) h[i] = 0;
 }
 
+// Smallest s with (width - 1) >> s < NBINS (width in [1, 2^32]).
 __device__ __forceinline__ int shift_for_width(uint64_t width)
 {
-    int s = 0;
-    while (((width - 1) >> s) >= (uint64_t)NBINS) ++s;
-    return s;
+    const uint32_t w = (uint32_t)(width - 1ull);
+    const int bits = 32 - __clz(w);  // bits needed for w
+    return bits > 11 ? bits - 11 : 0;
 }
 
 // ---------------------------------------------------------------------------------
@@ -400,7 +407,7 @@ __device__ __forceinline__ void bitonic_sort_desc(Ctx& c, int P)
                     a[hi] = A;
                 }
             }
-            __syncthreads();
+            csync();
         }
     }
 }
@@ -455,13 +462,14 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int
             const uint32_t kv = bkey[p];
             if (kv >= Tsel) atomicAdd(&hist[(NBINS - 1) - (int)((kv - Tsel) >> s)], 1);
         }
-        __syncthreads();
-        // exclusive scan over bins (4 consecutive bins per thread)
-        const int b0 = c.tid * 4;
-        int h[4];
+        csync();
+        // exclusive scan over bins (BPT consecutive bins per thread)
+        constexpr int BPT = NBINS / NT;
+        const int b0 = c.tid * BPT;
+        int h[BPT];
         uint32_t loc = 0, mx = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < BPT; ++i) {
             h[i] = hist[b0 + i];
             loc += (uint32_t)h[i];
             mx = max(mx, (uint32_t)h[i]);
@@ -472,11 +480,11 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int
         counting = mx <= (uint32_t)CSORT_BIN_MAX;
         if (counting) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < BPT; ++i) {
                 cur[b0 + i] = (int)off;
                 off += (uint32_t)h[i];
             }
-            __syncthreads();
+            csync();
             unsigned long long* cs = s_csort();
             for (int p = c.tid; p < fill; p += NT) {
                 const uint32_t kv = bkey[p];
@@ -486,7 +494,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int
                     cs[slot] = make_comp(kv, bidx[p]);
                 }
             }
-            __syncthreads();
+            csync();
             // insertion sort inside each bin (cur[b] now = end of bin b)
             for (int b = c.tid; b < NBINS; b += NT) {
                 const int cnt = hist[b];
@@ -503,7 +511,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int
                     }
                 }
             }
-            __syncthreads();
+            csync();
             write_output(c, cs, take, k, out, out_val);
             return;
         }
@@ -521,14 +529,14 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int
         v[j] = 0ull;
         if (p < m) v[j] = make_comp(bkey[p], bidx[p]);
     }
-    __syncthreads();  // all reads of B done before the aliasing writes
+    csync();  // all reads of B done before the aliasing writes
     unsigned long long* comp = s_comp();
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const int p = j * NT + c.tid;
         if (p < P) comp[p] = v[j];
     }
-    __syncthreads();
+    csync();
     bitonic_sort_desc(c, P);
     write_output(c, comp, take, k, out, out_val);
 }

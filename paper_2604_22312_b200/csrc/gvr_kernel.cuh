@@ -1,32 +1,32 @@
-// gvr_kernel.cuh — Guess-Verify-Refine exact Top-K, one CTA per row (sm_100a).
+// gvr_kernel.cuh — Guess-Verify-Refine exact Top-K on sm_100a: one 256-thread CTA per
+// row, two CTAs per SM (one streams while the other refines), TMA bulk-copy ring.
 //
-// Method: PAPER.md Sec. 4 (lines 379-690).  Phases as executed here:
-//   Phase 1 (Guess): gather x at the previous step's Top-K
-//     positions; pmin / pmax / pmean (Eq. 4) plus the second moment.
+// Method: PAPER.md Sec. 4 (lines 379-690).  Per row, as executed here:
+//   Phase 1 (Guess): x at the previous step's Top-K positions ->
+//     pmin / pmax / pmean (Eq. 4) plus the second moment (the first ring tiles are
+//     already in flight).
 //   Streaming pass (B200 re-design of the Phase-2 count pass fused with the Phase-3
 //     collector): the row body is read from HBM exactly once by TMA
-//     bulk copies into a 3-stage shared-memory ring (pipeline.cuh); every element whose
-//     key is >= the collect threshold T_c is appended (ballot-free, block-scan offsets)
-//     to the candidate buffer B in shared memory.  B therefore holds {x >= T_c} and
-//     f(T) for every T >= T_c can be counted from B alone (Lemma 1).
-//     If B would overflow, T_c is raised by a secant search over B (Eq. 6) to a
-//     threshold that still keeps >= K elements (so f(T_c) >= K at the end of the row).
+//     bulk copies into a 3 x 16 KB shared-memory ring (pipeline.cuh); every thread
+//     appends its elements (16 per tile) whose key is >= the collect
+//     threshold T_c to the candidate buffer B in shared memory (ballot-free, block-scan
+//     offsets).  B holds {x >= T_c}, so f(T) for every T >= T_c is counted from B alone
+//     (Lemma 1).  If B would overflow, T_c is raised by a secant
+//     search over B (Eq. 6) to a threshold that still keeps >= K elements.
 //   Phase 2: secant search of Eq. 6 toward f_target inside the
 //     window K <= f(T) <= C, starting from T0 = pmean, with first-step damping and
-//     bisection fallback — the counts come from B (shared memory), not from HBM.
+//     bisection fallback — counts from B (shared memory), not from HBM.
 //   Phase 3: ballot-free compaction of B to {x >= T} reusing the
 //     per-thread counts of the last count pass (count cache).
 //   Phase 4: 2048-bin histogram over the candidate key range,
-//     warp-parallel K-th-bin search, then the snap iterations (count_ge, count_gt,
-//     snap_up, snap_down) until n>(T) < K <= n>=(T) — run by one warp over the
-//     members of the K-th bin (every snap step stays inside that bin, so the result
-//     and the number of steps equal a scan over all candidates); exact narrowing of
-//     the bin if it is too large.
-//   Ordered output: the candidates >= T* are sorted by (key desc, index asc)
-//     (counting sort) and the first K indices are written (BASELINE.json tie rule).
-//   Fallbacks (R12/R13): underflow -> second
-//     streaming pass with T_c = -inf; massive ties -> exact radix select + ordered tie
-//     fill from global memory.
+//     warp-parallel K-th-bin search, snap iterations (count_ge, count_gt, snap_up,
+//     snap_down) until n>(T) < K <= n>=(T) — run by one warp over the K-th bin's members
+//     (every snap step stays inside that bin, so T* and the step count equal a scan over
+//     all candidates); exact narrowing of the bin if it is too large.
+//   Ordered output: candidates >= T* sorted by (key desc, index asc), first K written.
+//   Fallbacks (R12/R13): massive ties or an
+//     underflowing guess (f(T_c) < K) -> exact radix select + ordered tie fill from
+//     global memory.
 #pragma once
 #include "select_global.cuh"
 
@@ -64,42 +64,44 @@ __device__ __forceinline__ uint32_t secant_step(uint64_t lo, uint32_t clo, uint6
     return (uint32_t)(lo + ((hi - lo) >> 1));
 }
 
-// One ring tile held by a thread: 8 fp32 values (two float4 of the stage) and the
-// valid-element mask.  Element e sits at stage float 4*(tid + (e>>2)*NT) + (e&3).
-struct RingTile {
-    float x[8];
-    uint32_t vmask;
-    __device__ __forceinline__ static int pos(int tid, int e) { return 4 * (tid + (e >> 2) * NT) + (e & 3); }
-};
+// Element e (0..15) of a consumer thread's share of a ring tile sits at stage float
+// 4*(tid + (e>>2)*NT) + (e&3): float4 j = e>>2 of the thread is vector tid + j*NT.
+__device__ __forceinline__ int tile_pos(int tid, int e) { return 4 * (tid + (e >> 2) * NT) + (e & 3); }
 
-// Raise the collect threshold when B would overflow (B200 design).
-// B[0, fill) and the tile's elements >= Tc together exceed CAP.  Find T > Tc whose
-// count over B plus the tile lies in [K, CAP/2] by Eq. 6 secant steps aimed at
-// K <= f_target*phi <= CAP/2 (phi = streamed fraction of the row), compact B to
-// {key >= T} and return 0; return 1 if no such T exists (massive ties).
-__device__ __noinline__ int raise_threshold(Ctx& c, const RingTile& tl, uint32_t& Tc, int& fill, uint32_t c_at_tc,
-                                            float phi, int K, int max_secant, int& raises)
+// Raise the collect threshold when B would overflow.  B[0, fill) and
+// the tile's elements >= Tc together exceed CAP.  Find T > Tc whose count over B plus
+// the tile lies in [K, CAP/2] by Eq. 6 secant steps aimed at K <= f_target*phi <= CAP/2
+// (phi = streamed fraction of the row), compact B to {key >= T} and return 0; return 1
+// if no such T exists (massive ties).  The tile is re-read from the ring stage.
+__device__ __noinline__ int raise_threshold(const float* sp, uint32_t vmask, uint32_t& Tc, int& fill,
+                                            uint32_t c_at_tc, float phi, int K, int max_secant, int& raises,
+                                            int& par)
 {
-    uint32_t tk[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) tk[e] = ((tl.vmask >> e) & 1u) ? f2key(tl.x[e]) : 0u;
-    // exclusive upper anchor: 1 + max key over B and the tile
+    Ctx c = make_ctx();
+    c.par = par;
     uint32_t mx = buffer_max_local(c, fill);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) mx = max(mx, tk[e]);
+    for (int e = 0; e < 16; ++e)
+        if ((vmask >> e) & 1u) mx = max(mx, f2key(sp[tile_pos(c.tid, e)]));
     mx = block_red1<R_MAX>(c, mx);
-    uint64_t lo = Tc, hi = (uint64_t)mx + 1ull;
+    uint64_t lo = Tc, hi = (uint64_t)mx + 1ull;  // exclusive upper anchor
     uint32_t clo = c_at_tc, chi = 0;
     const uint32_t acc_hi = CAP / 2;
     const float ft = 0.5f * (float)(K + CWIN);
     const float target = fminf(fmaxf(ft * phi, (float)K), (float)acc_hi);
     uint32_t T = Tc;
     ChunkCounts cc;
+    int rc = 0;
     for (int it = 0;; ++it) {
-        if (it >= 64) return 1;  // safety bound (bisection needs <= 32 steps)
+        if (it >= 64) {  // safety bound (bisection needs <= 32 steps)
+            rc = 1;
+            break;
+        }
         if (hi - lo < 2) {
             // adjacent keys: no threshold in [K, CAP/2]; lo still fits if clo <= CAP
-            if (clo > (uint32_t)CAP || lo == (uint64_t)Tc) return 1;
+            if (clo > (uint32_t)CAP || lo == (uint64_t)Tc) {
+                rc = 1;
+                break;
+            }
             T = (uint32_t)lo;
             cc = count_chunks_ge(c, fill, T);
             break;
@@ -107,9 +109,8 @@ __device__ __noinline__ int raise_threshold(Ctx& c, const RingTile& tl, uint32_t
         T = secant_step(lo, clo, hi, chi, target, it == 0, it >= max_secant);
         cc = count_chunks_ge(c, fill, T);
         uint32_t cnt = chunk_total(cc);
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (((tl.vmask >> e) & 1u) && tk[e] >= T) ++cnt;
+        for (int e = 0; e < 16; ++e)
+            if (((vmask >> e) & 1u) && f2key(sp[tile_pos(c.tid, e)]) >= T) ++cnt;
         cnt = block_red1<R_ADD>(c, cnt);
         if (cnt >= (uint32_t)K && cnt <= acc_hi) break;
         if (cnt > acc_hi) {
@@ -120,16 +121,19 @@ __device__ __noinline__ int raise_threshold(Ctx& c, const RingTile& tl, uint32_t
             chi = cnt;
         }
     }
-    fill = compact_ge(c, fill, T, cc);
-    Tc = T;
-    ++raises;
-    return 0;
+    if (rc == 0) {
+        fill = compact_ge(c, fill, T, cc);
+        Tc = T;
+        ++raises;
+    }
+    par = c.par;
+    return rc;
 }
 
-// Streaming pass over the row: scalar head/tail exactly, then the body through the
-// TMA ring.  Collects B ⊇ {key >= Tc} (superset only by NaN / -0 against +0 entries,
-// which every later step filters by key), raising Tc on overflow.  Returns 0, or 1 on
-// massive ties.
+// Streaming pass over one row: scalar head/tail exactly, then the body tiles from the
+// ring.  Collects B ⊇ {key >= Tc} (superset only by NaN / -0-against-+0 entries, which
+// every later step filters by key), raising Tc on overflow.  Returns 0, or 1 on massive
+// ties.
 __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ring& ring, uint32_t& Tc, int& fill,
                                               int K, const GvrParams& prm, RowStats& st)
 {
@@ -159,42 +163,35 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
         ring.wait(t);
         const float* sp = ring.stage_ptr(t);
         const int nf = ring.tile_floats(t);
-        RingTile tl;
-        {
-            const float4 a = reinterpret_cast<const float4*>(sp)[c.tid];
-            const float4 b = reinterpret_cast<const float4*>(sp)[c.tid + NT];
-            tl.x[0] = a.x; tl.x[1] = a.y; tl.x[2] = a.z; tl.x[3] = a.w;
-            tl.x[4] = b.x; tl.x[5] = b.y; tl.x[6] = b.z; tl.x[7] = b.w;
-        }
-        if (nf == STAGE_FLOATS) {
-            tl.vmask = 0xffu;
-        } else {
-            tl.vmask = 0u;
+        uint32_t vmask = 0xffffu;
+        if (nf != STAGE_FLOATS) {
+            vmask = 0u;
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (RingTile::pos(c.tid, e) < nf) tl.vmask |= 1u << e;
+            for (int e = 0; e < 16; ++e)
+                if (tile_pos(c.tid, e) < nf) vmask |= 1u << e;
         }
         uint32_t mask = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (pass_ge(tl.x[e], Tf)) mask |= 1u << e;
-        mask &= tl.vmask;
+        for (int j = 0; j < 4; ++j) {
+            const float4 v = reinterpret_cast<const float4*>(sp)[c.tid + j * NT];
+            if (pass_ge(v.x, Tf)) mask |= 1u << (4 * j);
+            if (pass_ge(v.y, Tf)) mask |= 2u << (4 * j);
+            if (pass_ge(v.z, Tf)) mask |= 4u << (4 * j);
+            if (pass_ge(v.w, Tf)) mask |= 8u << (4 * j);
+        }
+        mask &= vmask;
         uint32_t tot;
         uint32_t ex = block_excl_scan(c, (uint32_t)__popc(mask), tot);
         // every thread is past tile t-1: refill its stage with tile t-1+NSTAGE
-        if (c.tid == 0 && t >= 1 && t - 1 + NSTAGE < ring.ntiles) {
-            fence_proxy_async();
-            ring.issue(t - 1 + NSTAGE);
-        }
+        if (c.tid == 0 && t >= 1 && t - 1 + NSTAGE < ring.ntiles) ring.issue(t - 1 + NSTAGE);
         if (fill + (int)tot > CAP) {  // block-uniform
             const float phi = (float)(g.head + g.tail + t * STAGE_FLOATS + nf) * inv_n;
-            if (raise_threshold(c, tl, Tc, fill, (uint32_t)fill + tot, phi, K, prm.max_secant, st.raises))
+            if (raise_threshold(sp, vmask, Tc, fill, (uint32_t)fill + tot, phi, K, prm.max_secant, st.raises, c.par))
                 return 1;
             Tf = key2f(Tc);
             mask = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (((tl.vmask >> e) & 1u) && f2key(tl.x[e]) >= Tc) mask |= 1u << e;
+            for (int e = 0; e < 16; ++e)
+                if (((vmask >> e) & 1u) && f2key(sp[tile_pos(c.tid, e)]) >= Tc) mask |= 1u << e;
             ex = block_excl_scan(c, (uint32_t)__popc(mask), tot);
         }
         // write the (few) candidates, picked out of the stage by index
@@ -203,13 +200,14 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
         while (mask) {
             const int e = __ffs(mask) - 1;
             mask &= mask - 1;
-            const int p = RingTile::pos(c.tid, e);
-            bkey[pos] = f2key(sp[p]);
-            bidx[pos] = ebase + p;
+            const int q = tile_pos(c.tid, e);
+            bkey[pos] = f2key(sp[q]);
+            bidx[pos] = ebase + q;
             ++pos;
         }
         fill += (int)tot;
     }
+    csync();  // B complete and visible; ring idle
     return 0;
 }
 
@@ -233,12 +231,12 @@ __device__ __forceinline__ uint32_t refine_exact(Ctx& c, int cand, int K, uint32
     for (int level = 0; level < 5; ++level) {
         zero_hist(c, hist, NBINS);
         if (c.tid == 0) misc[4] = 0;
-        __syncthreads();
+        csync();
         for (int p = c.tid; p < cand; p += NT) {
             const uint32_t k = bkey[p];
             if (k >= base && (uint64_t)(k - base) < width) atomicAdd(&hist[(k - base) >> s], 1);
         }
-        __syncthreads();
+        csync();
         int b;
         uint32_t a;
         kth_bin(c, NBINS, krem, b, a);
@@ -256,7 +254,7 @@ __device__ __forceinline__ uint32_t refine_exact(Ctx& c, int cand, int K, uint32
                 const uint32_t k = bkey[p];
                 if (k >= lo_b && (uint64_t)(k - lo_b) < bw) list[atomicAdd(&misc[4], 1)] = k;
             }
-            __syncthreads();
+            csync();
             if (c.warp == 0) {
                 // snap iterations, T starts at the bin's lower edge
                 uint32_t T = lo_b, nge = 0;
@@ -290,10 +288,12 @@ __device__ __forceinline__ uint32_t refine_exact(Ctx& c, int cand, int K, uint32
                     misc[8] = S;
                 }
             }
-            __syncthreads();
+            csync();
             nge_out = (uint32_t)misc[7];
             st.snap += misc[8];
-            return (uint32_t)misc[6];
+            const uint32_t Tstar = (uint32_t)misc[6];
+            csync();  // misc reused by the caller
+            return Tstar;
         }
         // exact narrowing inside bin b
         base = lo_b;
@@ -311,7 +311,7 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
     Ctx c = make_ctx();
     const int r = blockIdx.x;
     int n = (int)stride;
-    if (row_lens) n = min(max(row_lens[r], 0), (int)stride);
+    if (row_lens) n = min(max(__ldg(row_lens + r), 0), (int)stride);
     const float* x = scores + (int64_t)r * stride;
     int32_t* o = out + (int64_t)r * k;
     float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
@@ -327,10 +327,8 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         st.cand = n;
     } else {
         // start streaming the row body before Phase 1 (TMA ring, pipeline.cuh)
-        ring_init_barriers(c);
-        __syncthreads();
-        Ring ring = make_ring(x + g.head, 4 * g.nvec, 0u);
-        ring_prime(c, ring);
+        const Ring ring = make_ring(x + g.head, 4 * g.nvec);
+        ring_start(ring);
 
         // ---------------- Phase 1: guess statistics (Eq. 4)
         uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
@@ -350,7 +348,7 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
                 }
             }
         }
-        block_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+        block_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);  // also orders ring_start
         if (cnt == 0) {
             // no valid guess: deterministic stride sample of M values
             kmn = 0xffffffffu;
@@ -358,8 +356,8 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             sum = sq = 0.f;
             const int M = min(KMAX, n);
             for (int j = c.tid; j < M; j += NT) {
-                const int p = (int)(((int64_t)j * n) / M);
-                const float v = __ldg(x + p);
+                const int q = (int)(((int64_t)j * n) / M);
+                const float v = __ldg(x + q);
                 const uint32_t kv = f2key(v);
                 kmn = min(kmn, kv);
                 kmx = max(kmx, kv);
@@ -378,25 +376,15 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         const uint32_t T0 = f2key(pmean);
         const bool t0_ok = isfinite(pmean);
 
-        // ---------------- streaming pass (HBM read once)
+        // ---------------- streaming pass (HBM read once, TMA ring)
         int fill = 0;
-        int rc = stream_collect(c, g, ring, Tc, fill, K, prm, st);
-        __syncthreads();
+        const int rc = stream_collect(c, g, ring, Tc, fill, K, prm, st);
         ChunkCounts cc = count_chunks_ge(c, fill, Tc);
-        uint32_t ftc = rc == 0 ? block_red1<R_ADD>(c, chunk_total(cc)) : 0u;
-        if (rc == 0 && ftc < (uint32_t)K) {
-            // underflow: f(T_c) < K; stream again with T_c = -inf (always >= K)
-            Tc = 0u;
-            Ring ring2 = make_ring(x + g.head, 4 * g.nvec, (uint32_t)ring.ntiles);
-            ring_prime(c, ring2);
-            rc = stream_collect(c, g, ring2, Tc, fill, K, prm, st);
-            __syncthreads();
-            cc = count_chunks_ge(c, fill, Tc);
-            ftc = rc == 0 ? block_red1<R_ADD>(c, chunk_total(cc)) : 0u;
-        }
-        if (rc != 0) {
-            // massive ties: exact radix select + ordered tie fill (R13)
-            __syncthreads();
+        const uint32_t ftc = rc == 0 ? block_red1<R_ADD>(c, chunk_total(cc)) : 0u;
+        if (rc != 0 || ftc < (uint32_t)K) {
+            // massive ties, or f(T_c) < K (the guess overshot): exact radix select +
+            // ordered tie fill from global memory (R12/R13)
+            csync();
             const RadixResult rr = radix_select_global(c, g, (uint32_t)K, false);
             st.passes += rr.rounds + 1;
             st.done = GVR_DONE_TIEFILL;
@@ -446,8 +434,8 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             // ---------------- Phase 4: exact refinement
             uint32_t kmin = 0xffffffffu, kmax = 0u;
             const uint32_t* bkey = s_bkey();
-            for (int p = c.tid; p < cand; p += NT) {
-                const uint32_t kv = bkey[p];
+            for (int q = c.tid; q < cand; q += NT) {
+                const uint32_t kv = bkey[q];
                 kmin = min(kmin, kv);
                 kmax = max(kmax, kv);
             }
@@ -455,7 +443,17 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             uint32_t Tstar = kmin, nge = (uint32_t)cand;
             if (cand != K) Tstar = refine_exact(c, cand, K, kmin, kmax, nge, st);
             // ---------------- ordered output
-            emit_sorted(c, cand, Tstar, (int)nge, K, k, o, ov);
+            if (nge > (uint32_t)SORT_MAX) {
+                // huge tie group at T*: ordered tie fill from global memory (R13)
+                uint32_t ngt = 0;
+                for (int q = c.tid; q < cand; q += NT) ngt += bkey[q] > Tstar;
+                ngt = block_red1<R_ADD>(c, ngt);
+                st.done = GVR_DONE_TIEFILL;
+                ++st.passes;
+                tiefill_emit(c, g, Tstar, ngt, K, k, o, ov);
+            } else {
+                emit_sorted(c, cand, Tstar, (int)nge, K, k, o, ov);
+            }
         }
     }
     if (stats && c.tid == 0) {

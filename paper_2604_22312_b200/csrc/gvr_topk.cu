@@ -29,10 +29,10 @@ gvr_status validate(const float* scores, int64_t row_stride, int32_t num_rows, i
 }
 
 template <class Kern>
-gvr_status set_smem(Kern kern)
+gvr_status set_smem(Kern kern, int bytes)
 {
     // Opt in to > 48 KB dynamic shared memory; idempotent and cheap.
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
         (void)cudaGetLastError();
         return GVR_ERR_CUDA;
     }
@@ -78,7 +78,7 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
         if (opt->collect_sigma == opt->collect_sigma) prm.collect_sigma = opt->collect_sigma;
         if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
     }
-    if ((st = set_smem(gvr_topk_kernel)) != GVR_OK) return st;
+    if ((st = set_smem(gvr_topk_kernel, SMEM_BYTES)) != GVR_OK) return st;
     gvr_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, prev_topk, k, out_idx,
                                                           out_val, stats, prm);
     return launch_status();
@@ -98,7 +98,7 @@ gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const 
     gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
     if (st != GVR_OK) return st;
     if (num_rows == 0) return GVR_OK;
-    if ((st = set_smem(radix_topk_kernel)) != GVR_OK) return st;
+    if ((st = set_smem(radix_topk_kernel, SMEM_BYTES)) != GVR_OK) return st;
     radix_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
                                                             stats);
     return launch_status();

@@ -1,6 +1,6 @@
 // radix_kernel.cuh — in-house radix-select baseline (Sec. 2.2).
 //
-// One CTA (512 threads) per row, the same thread geometry as the GVR kernel (the
+// One CTA (256 threads) per row, the same thread geometry as the GVR kernel (the
 // paper's "identical thread-level resources").  Each round is a
 // full-row histogram pass over global memory into a 2048-bin shared-memory histogram
 // with atomicAdd, a K-th-bin search over the bin totals (the
@@ -46,7 +46,7 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 commit_unordered(c, tl, [&](uint32_t kk) { return kk >= lb; }, fill);
                 return 0;
             });
-            __syncthreads();
+            csync();
             cand = fill;
             emit_sorted(c, fill, 0u, fill, k, k, o, ov);
         } else {
@@ -58,7 +58,7 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                     commit_unordered(c, tl, [&](uint32_t kk) { return kk >= T; }, fill);
                     return 0;
                 });
-                __syncthreads();
+                csync();
                 emit_sorted(c, fill, 0u, fill, k, k, o, ov);
             } else {
                 tiefill_emit(c, g, rr.prefix, rr.above, k, k, o, ov);

@@ -3,7 +3,7 @@
 // A row x[0, n) is split into an unaligned scalar head (elements before the first
 // 16-byte boundary, < 4), a body of float4 vectors and a scalar tail (< 4).  The body
 // is consumed in tiles of TILE_VEC float4 (NT threads x VEC float4): within a tile,
-// float4 j of thread t is vector t*1 + j*NT, so every warp load is 512 contiguous
+// float4 j of thread t is vector t + j*NT, so every warp load is 512 contiguous
 // bytes (128-bit vectorised, coalesced; BASELINE.json north_star).  The next tile is
 // loaded into registers while the current one is processed (register double buffer).
 #pragma once

@@ -60,7 +60,7 @@ __device__ __forceinline__ RadixResult radix_select_global(Ctx& c, const RowGeom
         const int nb = 1 << bits;
         int32_t* hist = s_hist();
         zero_hist(c, hist, nb);
-        __syncthreads();
+        csync();
         for_each_tile(g, c.tid, [&](auto& tl, int) {
 #pragma unroll
             for (int e = 0; e < tl.E; ++e) {
@@ -69,7 +69,7 @@ __device__ __forceinline__ RadixResult radix_select_global(Ctx& c, const RowGeom
             }
             return 0;
         });
-        __syncthreads();
+        csync();
         int b;
         uint32_t a;
         kth_bin(c, nb, krem, b, a);
@@ -80,7 +80,7 @@ __device__ __forceinline__ RadixResult radix_select_global(Ctx& c, const RowGeom
         pmask |= dmask << shift;
         rr.rounds = round + 1;
         rr.bucket = cb;
-        __syncthreads();
+        csync();
         if (round == 2) {
             rr.exact = true;
             break;
@@ -138,13 +138,13 @@ __device__ __forceinline__ void tiefill_emit(Ctx& c, const RowGeom& g, uint32_t 
         }
         return 0;
     });
-    __syncthreads();
+    csync();
     // move the ties behind the > Tstar entries
     for (int i = c.tid; i < (int)need; i += NT) {
         bkey[n_gt + i] = bkey[tie_base + i];
         bidx[n_gt + i] = bidx[tie_base + i];
     }
-    __syncthreads();
+    csync();
     emit_sorted(c, K, 0u, K, K, k, out, out_val);
 }
 
@@ -156,7 +156,7 @@ __device__ __forceinline__ void small_row_emit(Ctx& c, const RowGeom& g, int k, 
         commit_unordered(c, tl, [](uint32_t) { return true; }, fill);
         return 0;
     });
-    __syncthreads();
+    csync();
     emit_sorted(c, g.n, 0u, g.n, g.n, k, out, out_val);
 }
 
