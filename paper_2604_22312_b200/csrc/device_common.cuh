@@ -244,6 +244,32 @@ __device__ __forceinline__ uint32_t block_excl_scan(Ctx& c, uint32_t v, uint32_t
     return before + x - v;
 }
 
+// Exclusive scan of v plus the block max of m, with one barrier.
+__device__ __forceinline__ uint32_t block_excl_scan_max(Ctx& c, uint32_t v, uint32_t m, uint32_t& total,
+                                                        uint32_t& mall)
+{
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (c.lane >= o) x += y;
+    }
+    const uint32_t wm = __reduce_max_sync(FULL, m);
+    uint32_t* s = s_red() + c.par * 4 * NW;
+    if (c.lane == 31) {
+        s[c.warp] = x;
+        s[NW + c.warp] = wm;
+    }
+    __syncwarp();
+    csync();
+    const uint32_t w = c.lane < NW ? s[c.lane] : 0u;
+    const uint32_t before = __reduce_add_sync(FULL, c.lane < c.warp ? w : 0u);
+    total = __reduce_add_sync(FULL, w);
+    mall = __reduce_max_sync(FULL, c.lane < NW ? s[NW + c.lane] : 0u);
+    c.par ^= 1;
+    return before + x - v;
+}
+
 // ---------------------------------------------------------------------------------
 // Candidate buffer B: slot p of chunk ch for thread t is ch*CHUNK + j*NT + t.  Counting
 // passes cache per-chunk counts (the "count cache" of PAPER.md:588-597, applied to the
@@ -259,10 +285,12 @@ __device__ __forceinline__ ChunkCounts count_chunks_ge(const Ctx& c, int fill, u
 #pragma unroll
     for (int ch = 0; ch < NCHUNK; ++ch) {
         uint32_t n = 0;
+        if (ch * CHUNK < fill) {  // block-uniform: skip empty chunks
 #pragma unroll
-        for (int j = 0; j < CHUNK_SLOTS; ++j) {
-            const int p = ch * CHUNK + j * NT + c.tid;
-            if (p < fill && bkey[p] >= T) ++n;
+            for (int j = 0; j < CHUNK_SLOTS; ++j) {
+                const int p = ch * CHUNK + j * NT + c.tid;
+                if (p < fill && bkey[p] >= T) ++n;
+            }
         }
         cc.c[ch] = n;
     }
@@ -441,20 +469,24 @@ __device__ __forceinline__ void write_output(const Ctx& c, const unsigned long l
 // offsets by one block scan, scatter with per-bin cursors, then an insertion sort of
 // the (few) entries that share a bin.  Falls back to the bitonic sort when the
 // selection or a bin is too large.
-__device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int n_sel, int take, int k,
-                                            int32_t* out, float* out_val)
+__device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uint32_t kmax_sel, int n_sel, int take,
+                                            int k, int32_t* out, float* out_val)
 {
     uint32_t* bkey = s_bkey();
     int32_t* bidx = s_bidx();
-    uint32_t kmx = 0;
-    for (int p = c.tid; p < fill; p += NT) {
-        const uint32_t kv = bkey[p];
-        if (kv >= Tsel) kmx = max(kmx, kv);
-    }
     int32_t* hist = s_hist();
     int32_t* cur = s_aux();
     zero_hist(c, hist, NBINS);
-    kmx = block_red1<R_MAX>(c, kmx);  // (barrier also orders the zeroing)
+    uint32_t kmx = kmax_sel;
+    if (kmx == 0u) {  // not known by the caller
+        for (int p = c.tid; p < fill; p += NT) {
+            const uint32_t kv = bkey[p];
+            if (kv >= Tsel) kmx = max(kmx, kv);
+        }
+        kmx = block_red1<R_MAX>(c, kmx);  // (barrier also orders the zeroing)
+    } else {
+        csync();
+    }
     const int s = shift_for_width((uint64_t)kmx - Tsel + 1ull);
     bool counting = n_sel <= CSORT_MAX;
     if (counting) {
@@ -475,8 +507,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, int
             mx = max(mx, (uint32_t)h[i]);
         }
         uint32_t tot;
-        uint32_t off = block_excl_scan(c, loc, tot);
-        mx = block_red1<R_MAX>(c, mx);
+        uint32_t off = block_excl_scan_max(c, loc, mx, tot, mx);
         counting = mx <= (uint32_t)CSORT_BIN_MAX;
         if (counting) {
 #pragma unroll

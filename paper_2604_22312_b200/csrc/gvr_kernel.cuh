@@ -134,14 +134,13 @@ __device__ __noinline__ int raise_threshold(const float* sp, uint32_t vmask, uin
 // ring.  Collects B ⊇ {key >= Tc} (superset only by NaN / -0-against-+0 entries, which
 // every later step filters by key), raising Tc on overflow.  Returns 0, or 1 on massive
 // ties.
-__device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ring& ring, uint32_t& Tc, int& fill,
-                                              int K, const GvrParams& prm, RowStats& st)
+__device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ring& ring, int t_start, uint32_t& Tc,
+                                              int& fill, int K, const GvrParams& prm, RowStats& st)
 {
     uint32_t* bkey = s_bkey();
     int32_t* bidx = s_bidx();
-    ++st.passes;
-    fill = 0;
-    {  // scalar head [0, head) and tail [body_end, n): <= 6 elements, exact key test
+    if (t_start == 0) {  // scalar head [0, head) and tail [body_end, n): <= 6 elements, exact key test
+        fill = 0;
         int i = -1;
         if (c.tid < g.head)
             i = c.tid;
@@ -159,7 +158,7 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
     }
     const float inv_n = 1.0f / (float)g.n;
     float Tf = key2f(Tc);
-    for (int t = 0; t < ring.ntiles; ++t) {
+    for (int t = t_start; t < ring.ntiles; ++t) {
         ring.wait(t);
         const float* sp = ring.stage_ptr(t);
         const int nf = ring.tile_floats(t);
@@ -209,6 +208,39 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
     }
     csync();  // B complete and visible; ring idle
     return 0;
+}
+
+// Capture the scalar head/tail and the whole first ring tile into B unfiltered (the
+// collect threshold is not known yet: Phase 1's gathers are still in flight).  Tile 0
+// keeps its stage layout, so B[0, nf0) is contiguous; the <= 6 scalars follow.
+// Returns the fill.
+__device__ __forceinline__ int capture_first_tile(Ctx& c, const RowGeom& g, const Ring& ring)
+{
+    uint32_t* bkey = s_bkey();
+    int32_t* bidx = s_bidx();
+    int nf0 = 0;
+    if (ring.ntiles > 0) {
+        ring.wait(0);
+        nf0 = ring.tile_floats(0);
+        const float4* sp = reinterpret_cast<const float4*>(ring.stage_ptr(0));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int v = c.tid + j * NT;
+            if (4 * v < nf0) {
+                const float4 f = sp[v];
+                reinterpret_cast<uint4*>(bkey)[v] = make_uint4(f2key(f.x), f2key(f.y), f2key(f.z), f2key(f.w));
+                const int i0 = g.head + 4 * v;
+                reinterpret_cast<int4*>(bidx)[v] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+            }
+        }
+    }
+    const int ns = g.head + g.tail;  // <= 6
+    if (c.tid < ns) {
+        const int i = c.tid < g.head ? c.tid : g.body_end + (c.tid - g.head);
+        bkey[nf0 + c.tid] = f2key(__ldg(g.x + i));
+        bidx[nf0 + c.tid] = i;
+    }
+    return nf0 + ns;
 }
 
 // Phase 4 over the candidates B[0, cand): returns T*, the exact
@@ -331,24 +363,46 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         ring_start(ring);
 
         // ---------------- Phase 1: guess statistics (Eq. 4)
-        uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
-        float sum = 0.f, sq = 0.f;
-        if (prev) {
-            const int32_t* pr = prev + (int64_t)r * k;
-            for (int j = c.tid; j < k; j += NT) {
-                const int p = pr[j];
-                if (p >= 0 && p < n) {
-                    const float v = __ldg(x + p);
-                    const uint32_t kv = f2key(v);
-                    kmn = min(kmn, kv);
-                    kmx = max(kmx, kv);
-                    ++cnt;
-                    sum += v;
-                    sq += v * v;
+        // The gathers are issued now and consumed after the first ring tile has been
+        // captured, so their latency overlaps the first TMA transfer.
+        constexpr int GPT = KMAX / NT;  // guesses per thread
+        float gv[GPT];
+        uint32_t gok = 0;
+        {
+            int32_t gi[GPT];
+            const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
+#pragma unroll
+            for (int j = 0; j < GPT; ++j) {
+                const int q = c.tid + j * NT;
+                gi[j] = -1;
+                if (pr && q < k) asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(gi[j]) : "l"(pr + q));
+            }
+#pragma unroll
+            for (int j = 0; j < GPT; ++j) {
+                gv[j] = 0.f;
+                if (gi[j] >= 0 && gi[j] < n) {
+                    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(gv[j]) : "l"(x + gi[j]));
+                    gok |= 1u << j;
                 }
             }
         }
-        block_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);  // also orders ring_start
+        csync();  // ring barriers initialised before anyone waits on them
+        int fill = capture_first_tile(c, g, ring);
+        uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
+        float sum = 0.f, sq = 0.f;
+#pragma unroll
+        for (int j = 0; j < GPT; ++j) {
+            if ((gok >> j) & 1u) {
+                const float v = gv[j];
+                const uint32_t kv = f2key(v);
+                kmn = min(kmn, kv);
+                kmx = max(kmx, kv);
+                ++cnt;
+                sum += v;
+                sq += v * v;
+            }
+        }
+        block_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
         if (cnt == 0) {
             // no valid guess: deterministic stride sample of M values
             kmn = 0xffffffffu;
@@ -377,8 +431,12 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         const bool t0_ok = isfinite(pmean);
 
         // ---------------- streaming pass (HBM read once, TMA ring)
-        int fill = 0;
-        const int rc = stream_collect(c, g, ring, Tc, fill, K, prm, st);
+        ++st.passes;
+        if (Tc != 0u) {  // apply T_c to the captured first tile
+            const ChunkCounts c0 = count_chunks_ge(c, fill, Tc);
+            fill = compact_ge(c, fill, Tc, c0);
+        }
+        const int rc = stream_collect(c, g, ring, 1, Tc, fill, K, prm, st);
         ChunkCounts cc = count_chunks_ge(c, fill, Tc);
         const uint32_t ftc = rc == 0 ? block_red1<R_ADD>(c, chunk_total(cc)) : 0u;
         if (rc != 0 || ftc < (uint32_t)K) {
@@ -452,7 +510,7 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
                 ++st.passes;
                 tiefill_emit(c, g, Tstar, ngt, K, k, o, ov);
             } else {
-                emit_sorted(c, cand, Tstar, (int)nge, K, k, o, ov);
+                emit_sorted(c, cand, Tstar, kmax, (int)nge, K, k, o, ov);
             }
         }
     }

@@ -48,7 +48,7 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             });
             csync();
             cand = fill;
-            emit_sorted(c, fill, 0u, fill, k, k, o, ov);
+            emit_sorted(c, fill, 0u, 0u, fill, k, k, o, ov);
         } else {
             cand = (int)(rr.above + rr.bucket);
             if (rr.above + rr.bucket <= (uint32_t)SORT_MAX) {
@@ -59,7 +59,7 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                     return 0;
                 });
                 csync();
-                emit_sorted(c, fill, 0u, fill, k, k, o, ov);
+                emit_sorted(c, fill, 0u, 0u, fill, k, k, o, ov);
             } else {
                 tiefill_emit(c, g, rr.prefix, rr.above, k, k, o, ov);
             }

@@ -145,7 +145,7 @@ __device__ __forceinline__ void tiefill_emit(Ctx& c, const RowGeom& g, uint32_t 
         bidx[n_gt + i] = bidx[tie_base + i];
     }
     csync();
-    emit_sorted(c, K, 0u, K, K, k, out, out_val);
+    emit_sorted(c, K, 0u, 0u, K, K, k, out, out_val);
 }
 
 // Rows with len <= k: every element, sorted, then -1 padding (R5).
@@ -157,7 +157,7 @@ __device__ __forceinline__ void small_row_emit(Ctx& c, const RowGeom& g, int k, 
         return 0;
     });
     csync();
-    emit_sorted(c, g.n, 0u, g.n, g.n, k, out, out_val);
+    emit_sorted(c, g.n, 0u, 0u, g.n, g.n, k, out, out_val);
 }
 
 }  // namespace gvr

@@ -34,3 +34,32 @@ ti = sum(v[0] for v in agg.values()); ts = sum(v[1] for v in agg.values())
 print(f"mapped {len(line_of)} sass offsets; total instr {ti:.3e} samples {ts:.0f}")
 for (fn, l), (i, s) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
     print(f"{fn:22s}:{l:<5d} instr {100*i/ti:5.1f}%  samples {100*s/ts:5.1f}%")
+
+# ---- per-function breakdown (by line ranges of function definitions)
+def func_ranges(path):
+    import re
+    rng = []
+    try:
+        src = open(path).read().splitlines()
+    except OSError:
+        return rng
+    starts = [(i + 1, m.group(1)) for i, l in enumerate(src)
+              for m in [re.match(r"^(?:template\s*<[^>]*>\s*)?(?:__device__|__global__)[^(]*?\b(\w+)\s*\(", l)] if m]
+    for j, (ln, name) in enumerate(starts):
+        end = starts[j + 1][0] - 1 if j + 1 < len(starts) else len(src)
+        rng.append((ln, end, name))
+    return rng
+csrc = os.path.join(os.path.dirname(os.path.abspath(lib)), "csrc")
+fr = {f: func_ranges(os.path.join(csrc, f)) for f in os.listdir(csrc)}
+byf = collections.defaultdict(lambda: [0.0, 0.0])
+for (fn, l), (i, s) in agg.items():
+    name = fn
+    for a, b, nm in fr.get(fn, []):
+        if a <= l <= b:
+            name = f"{fn}:{nm}"
+            break
+    byf[name][0] += i
+    byf[name][1] += s
+print("\n-- by function --")
+for nm, (i, s) in sorted(byf.items(), key=lambda kv: -kv[1][1])[:25]:
+    print(f"{nm:45s} instr {100*i/ti:5.1f}%  samples {100*s/ts:5.1f}%")
