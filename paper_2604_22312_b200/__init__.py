@@ -57,6 +57,7 @@ def _load():
         "gvr_workspace_create": [i32, i64, i32, ctypes.POINTER(vp)],
         "gvr_workspace_destroy": [vp],
         "gvr_topk_batched_host": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
+        "gvr_topk_phase_timing": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -138,6 +139,20 @@ def topk_ex(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, values: 
     _check(_load().gvr_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
                                        _ptr(out), _stream_ptr(stream), opt, _ptr(val), _ptr(st)))
     return out, val, st
+
+
+PHASES = ("phase1", "stream", "phase2_3", "phase4", "output")
+
+
+def topk_phase_timing(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None):
+    """GVR Top-K plus per-row clock64 stamps [R, 6] (start, end of Phase 1, stream,
+    Phases 2-3, Phase 4, end) — the paper's per-phase breakdown (Table 8)."""
+    torch = _torch()
+    R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
+    ts = torch.zeros((R, 6), dtype=torch.int64, device=scores.device)
+    _check(_load().gvr_topk_phase_timing(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
+                                         _ptr(out), _stream_ptr(stream), _ptr(ts)))
+    return out, ts
 
 
 def radix_topk(scores, k: int = MAX_K, row_lens=None, out=None, stream=None):

@@ -28,7 +28,7 @@ constexpr int VEC = 4;                  // float4 loads per thread per register 
 constexpr int TILE_VEC = NT * VEC;      // float4s per register tile (8192 elements)
 constexpr int SORT_MAX = 4096;          // largest bitonic ordered-output sort (64-bit composites)
 constexpr int CSORT_MAX = 4096;         // largest counting-sort ordered output
-constexpr int CSORT_BIN_MAX = 32;       // counting sort: largest bin sorted by insertion
+constexpr int CSORT_BIN_MAX = 32;       // counting sort: largest bin ranked in place
 constexpr int LIST_MAX = 4096;          // Phase 4: largest K-th-bin member list
 constexpr int RADIX_EARLY = 2048;       // radix early exit
 constexpr unsigned FULL = 0xffffffffu;
@@ -466,8 +466,8 @@ __device__ __forceinline__ void write_output(const Ctx& c, const unsigned long l
 // Emit the entries of B[0, fill) with key >= Tsel (n_sel of them, n_sel <= SORT_MAX),
 // sorted, as the row's first `take` outputs, then -1 padding up to k.
 // Counting sort: a 2048-bin histogram over [Tsel, kmax] (bin 0 = highest keys), bin
-// offsets by one block scan, scatter with per-bin cursors, then an insertion sort of
-// the (few) entries that share a bin.  Falls back to the bitonic sort when the
+// offsets by one block scan, scatter with per-bin cursors, then every entry is ranked
+// among the (few) entries that share its bin, in parallel.  Falls back to the bitonic sort when the
 // selection or a bin is too large.
 __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uint32_t kmax_sel, int n_sel, int take,
                                             int k, int32_t* out, float* out_val)
@@ -512,7 +512,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
         if (counting) {
 #pragma unroll
             for (int i = 0; i < BPT; ++i) {
-                cur[b0 + i] = (int)off;
+                cur[b0 + i] = (int)off;  // bin start; becomes the bin end after the scatter
                 off += (uint32_t)h[i];
             }
             csync();
@@ -526,24 +526,29 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
                 }
             }
             csync();
-            // insertion sort inside each bin (cur[b] now = end of bin b)
-            for (int b = c.tid; b < NBINS; b += NT) {
+            // rank every entry inside its (small) bin in parallel: final position =
+            // bin start + #entries of the bin with a larger composite; B is free now
+            int32_t* fidx = s_bidx();
+            float* fval = reinterpret_cast<float*>(s_bkey());
+            for (int j = c.tid; j < n_sel; j += NT) {
+                const unsigned long long v = cs[j];
+                const int b = (NBINS - 1) - (int)((comp_key(v) - Tsel) >> s);
                 const int cnt = hist[b];
-                if (cnt > 1) {
-                    const int st = cur[b] - cnt;
-                    for (int i = st + 1; i < st + cnt; ++i) {
-                        const unsigned long long v = cs[i];
-                        int j = i - 1;
-                        while (j >= st && cs[j] < v) {
-                            cs[j + 1] = cs[j];
-                            --j;
-                        }
-                        cs[j + 1] = v;
-                    }
+                const int st = cur[b] - cnt;
+                int rank = 0;
+                for (int i = st; i < st + cnt; ++i) rank += cs[i] > v;
+                const int pos = st + rank;
+                if (pos < take) {
+                    fidx[pos] = comp_idx(v);
+                    fval[pos] = key2f(comp_key(v));
                 }
             }
             csync();
-            write_output(c, cs, take, k, out, out_val);
+            for (int j = c.tid; j < k; j += NT) {
+                const bool in = j < take;
+                out[j] = in ? fidx[j] : -1;
+                if (out_val) out_val[j] = in ? fval[j] : 0.f;
+            }
             return;
         }
     }

@@ -135,7 +135,8 @@ __device__ __noinline__ int raise_threshold(const float* sp, uint32_t vmask, uin
 // every later step filters by key), raising Tc on overflow.  Returns 0, or 1 on massive
 // ties.
 __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ring& ring, int t_start, uint32_t& Tc,
-                                              int& fill, int K, const GvrParams& prm, RowStats& st)
+                                              int& fill, int K, const GvrParams& prm, RowStats& st, uint32_t& kmax_local,
+                                              uint32_t& extras)
 {
     uint32_t* bkey = s_bkey();
     int32_t* bidx = s_bidx();
@@ -187,6 +188,7 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
             const float phi = (float)(g.head + g.tail + t * STAGE_FLOATS + nf) * inv_n;
             if (raise_threshold(sp, vmask, Tc, fill, (uint32_t)fill + tot, phi, K, prm.max_secant, st.raises, c.par))
                 return 1;
+            extras = 0;  // the compaction was exact
             Tf = key2f(Tc);
             mask = 0;
             for (int e = 0; e < 16; ++e)
@@ -200,13 +202,15 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
             const int e = __ffs(mask) - 1;
             mask &= mask - 1;
             const int q = tile_pos(c.tid, e);
-            bkey[pos] = f2key(sp[q]);
+            const uint32_t kv = f2key(sp[q]);
+            kmax_local = max(kmax_local, kv);
+            extras += kv < Tc;  // superset entry (NaN / -0 against +0)
+            bkey[pos] = kv;
             bidx[pos] = ebase + q;
             ++pos;
         }
         fill += (int)tot;
     }
-    csync();  // B complete and visible; ring idle
     return 0;
 }
 
@@ -214,7 +218,7 @@ __device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ri
 // collect threshold is not known yet: Phase 1's gathers are still in flight).  Tile 0
 // keeps its stage layout, so B[0, nf0) is contiguous; the <= 6 scalars follow.
 // Returns the fill.
-__device__ __forceinline__ int capture_first_tile(Ctx& c, const RowGeom& g, const Ring& ring)
+__device__ __forceinline__ int capture_first_tile(Ctx& c, const RowGeom& g, const Ring& ring, uint32_t& kmax_local)
 {
     uint32_t* bkey = s_bkey();
     int32_t* bidx = s_bidx();
@@ -228,7 +232,9 @@ __device__ __forceinline__ int capture_first_tile(Ctx& c, const RowGeom& g, cons
             const int v = c.tid + j * NT;
             if (4 * v < nf0) {
                 const float4 f = sp[v];
-                reinterpret_cast<uint4*>(bkey)[v] = make_uint4(f2key(f.x), f2key(f.y), f2key(f.z), f2key(f.w));
+                const uint4 kk = make_uint4(f2key(f.x), f2key(f.y), f2key(f.z), f2key(f.w));
+                kmax_local = max(kmax_local, max(max(kk.x, kk.y), max(kk.z, kk.w)));
+                reinterpret_cast<uint4*>(bkey)[v] = kk;
                 const int i0 = g.head + 4 * v;
                 reinterpret_cast<int4*>(bidx)[v] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
             }
@@ -237,7 +243,9 @@ __device__ __forceinline__ int capture_first_tile(Ctx& c, const RowGeom& g, cons
     const int ns = g.head + g.tail;  // <= 6
     if (c.tid < ns) {
         const int i = c.tid < g.head ? c.tid : g.body_end + (c.tid - g.head);
-        bkey[nf0 + c.tid] = f2key(__ldg(g.x + i));
+        const uint32_t kv = f2key(__ldg(g.x + i));
+        kmax_local = max(kmax_local, kv);
+        bkey[nf0 + c.tid] = kv;
         bidx[nf0 + c.tid] = i;
     }
     return nf0 + ns;
@@ -336,10 +344,17 @@ __device__ __forceinline__ uint32_t refine_exact(Ctx& c, int cand, int K, uint32
     return base;  // unreachable: s reaches 0 within 3 narrowing levels
 }
 
+// Phase timestamps: clock64() at phase boundaries, written by thread 0 when `phase_ts`
+// is non-null (the paper's -DGVR_PHASE_TIMING instrumentation).
+enum { TS_START = 0, TS_PHASE1, TS_STREAM, TS_PHASE23, TS_PHASE4, TS_END, TS_N };
+
 __global__ void __launch_bounds__(NT, 2)
 gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens,
-                const int32_t* prev, int k, int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm)
+                const int32_t* prev, int k, int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm,
+                long long* phase_ts)
 {
+    long long ts[TS_N] = {0, 0, 0, 0, 0, 0};
+    if (phase_ts) ts[TS_START] = clock64();
     Ctx c = make_ctx();
     const int r = blockIdx.x;
     int n = (int)stride;
@@ -387,7 +402,8 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             }
         }
         csync();  // ring barriers initialised before anyone waits on them
-        int fill = capture_first_tile(c, g, ring);
+        uint32_t kmax_local = 0u, extras = 0u;
+        int fill = capture_first_tile(c, g, ring, kmax_local);
         uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
         float sum = 0.f, sq = 0.f;
 #pragma unroll
@@ -431,18 +447,21 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         const bool t0_ok = isfinite(pmean);
 
         // ---------------- streaming pass (HBM read once, TMA ring)
+        if (phase_ts) ts[TS_PHASE1] = clock64();
         ++st.passes;
         if (Tc != 0u) {  // apply T_c to the captured first tile
             const ChunkCounts c0 = count_chunks_ge(c, fill, Tc);
             fill = compact_ge(c, fill, Tc, c0);
         }
-        const int rc = stream_collect(c, g, ring, 1, Tc, fill, K, prm, st);
-        ChunkCounts cc = count_chunks_ge(c, fill, Tc);
-        const uint32_t ftc = rc == 0 ? block_red1<R_ADD>(c, chunk_total(cc)) : 0u;
+        const int rc = stream_collect(c, g, ring, 1, Tc, fill, K, prm, st, kmax_local, extras);
+        uint32_t kmax = kmax_local;
+        block_red2<R_MAX, R_ADD>(c, kmax, extras);  // also: B complete and visible
+        const uint32_t ftc = rc == 0 ? (uint32_t)fill - extras : 0u;  // exact f(T_c)
+        if (phase_ts) ts[TS_STREAM] = clock64();
+        ChunkCounts cc;
         if (rc != 0 || ftc < (uint32_t)K) {
             // massive ties, or f(T_c) < K (the guess overshot): exact radix select +
             // ordered tie fill from global memory (R12/R13)
-            csync();
             const RadixResult rr = radix_select_global(c, g, (uint32_t)K, false);
             st.passes += rr.rounds + 1;
             st.done = GVR_DONE_TIEFILL;
@@ -453,8 +472,7 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             // ---------------- Phase 2: secant search over B
             uint32_t T = Tc;
             if (ftc > (uint32_t)CWIN) {
-                const uint32_t mx = block_red1<R_MAX>(c, buffer_max_local(c, fill));
-                uint64_t lo = Tc, hi = (uint64_t)mx + 1ull;
+                uint64_t lo = Tc, hi = (uint64_t)kmax + 1ull;  // kmax = max key in B
                 uint32_t clo = ftc, chi = 0;
                 const float target = 0.5f * (float)(K + CWIN);  // f_target
                 bool have_t0 = t0_ok && (uint64_t)T0 > lo && (uint64_t)T0 < hi;
@@ -487,24 +505,30 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             }
             // ---------------- Phase 3: ballot-free compaction
             int cand = fill;
-            if (T != Tc || ftc != (uint32_t)fill) cand = compact_ge(c, fill, T, cc);
-            st.cand = cand;
-            // ---------------- Phase 4: exact refinement (PAPER.md:614-657)
-            uint32_t kmin = 0xffffffffu, kmax = 0u;
-            const uint32_t* bkey = s_bkey();
-            for (int q = c.tid; q < cand; q += NT) {
-                const uint32_t kv = bkey[q];
-                kmin = min(kmin, kv);
-                kmax = max(kmax, kv);
+            if (T != Tc) {
+                cand = compact_ge(c, fill, T, cc);
+            } else if (extras != 0u) {
+                cc = count_chunks_ge(c, fill, T);
+                cand = compact_ge(c, fill, T, cc);
             }
-            block_red2<R_MIN, R_MAX>(c, kmin, kmax);
-            uint32_t Tstar = kmin, nge = (uint32_t)cand;
-            if (cand != K) Tstar = refine_exact(c, cand, K, kmin, kmax, nge, st);
+            st.cand = cand;
+            if (phase_ts) ts[TS_PHASE23] = clock64();
+            // ---------------- Phase 4: exact refinement (PAPER.md:614-657)
+            // every candidate key lies in [T, kmax] (kmax tracked while collecting)
+            uint32_t Tstar = T, nge = (uint32_t)cand;
+            if (cand != K) {
+                Tstar = refine_exact(c, cand, K, T, kmax, nge, st);
+            } else {
+                uint32_t kmin = 0xffffffffu;
+                for (int q = c.tid; q < cand; q += NT) kmin = min(kmin, s_bkey()[q]);
+                Tstar = block_red1<R_MIN>(c, kmin);
+            }
+            if (phase_ts) ts[TS_PHASE4] = clock64();
             // ---------------- ordered output
             if (nge > (uint32_t)SORT_MAX) {
                 // huge tie group at T*: ordered tie fill from global memory (R13)
                 uint32_t ngt = 0;
-                for (int q = c.tid; q < cand; q += NT) ngt += bkey[q] > Tstar;
+                for (int q = c.tid; q < cand; q += NT) ngt += s_bkey()[q] > Tstar;
                 ngt = block_red1<R_ADD>(c, ngt);
                 st.done = GVR_DONE_TIEFILL;
                 ++st.passes;
@@ -513,6 +537,10 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
                 emit_sorted(c, cand, Tstar, kmax, (int)nge, K, k, o, ov);
             }
         }
+    }
+    if (phase_ts && c.tid == 0) {
+        ts[TS_END] = clock64();
+        for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = ts[i];
     }
     if (stats && c.tid == 0) {
         gvr_row_stats s;

@@ -61,9 +61,9 @@ const char* gvr_status_string(gvr_status s)
 
 int32_t gvr_version(void) { return kVersion; }
 
-gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
-                               const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
-                               const gvr_options* opt, float* out_val, gvr_row_stats* stats)
+static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                             const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                             const gvr_options* opt, float* out_val, gvr_row_stats* stats, long long* phase_ts)
 {
     gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
     if (st != GVR_OK) return st;
@@ -80,8 +80,25 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
     }
     if ((st = set_smem(gvr_topk_kernel, SMEM_BYTES)) != GVR_OK) return st;
     gvr_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, prev_topk, k, out_idx,
-                                                          out_val, stats, prm);
+                                                          out_val, stats, prm, phase_ts);
     return launch_status();
+}
+
+gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                               const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                               const gvr_options* opt, float* out_val, gvr_row_stats* stats)
+{
+    return gvr_launch(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, opt, out_val, stats,
+                      nullptr);
+}
+
+gvr_status gvr_topk_phase_timing(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                                 const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                                 long long* phase_ts)
+{
+    if (!phase_ts && num_rows > 0) return GVR_ERR_INVALID_ARGUMENT;
+    return gvr_launch(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, nullptr, nullptr,
+                      nullptr, phase_ts);
 }
 
 gvr_status gvr_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
