@@ -463,9 +463,21 @@ __device__ __forceinline__ void write_output(const Ctx& c, const unsigned long l
     }
 }
 
+// Linear bin of d = key - Tsel over [0, range) with all NBINS bins in use:
+// (d * scale) >> 32 with scale = floor(2^32 * NBINS / range), monotone in d.
+__device__ __forceinline__ uint32_t bin_scale(uint64_t range)
+{
+    const unsigned long long q = (((unsigned long long)NBINS) << 32) / range;
+    return q > 0xffffffffull ? 0xffffffffu : (uint32_t)q;
+}
+__device__ __forceinline__ int lin_bin(uint32_t d, uint32_t scale)
+{
+    return min((int)(((uint64_t)d * scale) >> 32), NBINS - 1);
+}
+
 // Emit the entries of B[0, fill) with key >= Tsel (n_sel of them, n_sel <= SORT_MAX),
 // sorted, as the row's first `take` outputs, then -1 padding up to k.
-// Counting sort: a 2048-bin histogram over [Tsel, kmax] (bin 0 = highest keys), bin
+// Counting sort: a 2048-bin linear histogram over [Tsel, kmax] (bin 0 = highest keys), bin
 // offsets by one block scan, scatter with per-bin cursors, then every entry is ranked
 // among the (few) entries that share its bin, in parallel.  Falls back to the bitonic sort when the
 // selection or a bin is too large.
@@ -487,12 +499,12 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
     } else {
         csync();
     }
-    const int s = shift_for_width((uint64_t)kmx - Tsel + 1ull);
+    const uint32_t scale = bin_scale((uint64_t)kmx - Tsel + 1ull);
     bool counting = n_sel <= CSORT_MAX;
     if (counting) {
         for (int p = c.tid; p < fill; p += NT) {
             const uint32_t kv = bkey[p];
-            if (kv >= Tsel) atomicAdd(&hist[(NBINS - 1) - (int)((kv - Tsel) >> s)], 1);
+            if (kv >= Tsel) atomicAdd(&hist[(NBINS - 1) - lin_bin(kv - Tsel, scale)], 1);
         }
         csync();
         // exclusive scan over bins (BPT consecutive bins per thread)
@@ -520,7 +532,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
             for (int p = c.tid; p < fill; p += NT) {
                 const uint32_t kv = bkey[p];
                 if (kv >= Tsel) {
-                    const int b = (NBINS - 1) - (int)((kv - Tsel) >> s);
+                    const int b = (NBINS - 1) - lin_bin(kv - Tsel, scale);
                     const int slot = atomicAdd(&cur[b], 1);
                     cs[slot] = make_comp(kv, bidx[p]);
                 }
@@ -532,7 +544,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
             float* fval = reinterpret_cast<float*>(s_bkey());
             for (int j = c.tid; j < n_sel; j += NT) {
                 const unsigned long long v = cs[j];
-                const int b = (NBINS - 1) - (int)((comp_key(v) - Tsel) >> s);
+                const int b = (NBINS - 1) - lin_bin(comp_key(v) - Tsel, scale);
                 const int cnt = hist[b];
                 const int st = cur[b] - cnt;
                 int rank = 0;
