@@ -143,8 +143,17 @@ gvr_status gvr_topk_batched_host(const float* h_scores, int64_t row_stride,
 /* Static string for a status code (never NULL). */
 const char* gvr_status_string(gvr_status s);
 
+/* Text of the last CUDA error behind a GVR_ERR_CUDA returned on this host thread. */
+const char* gvr_last_cuda_error(void);
+
 /* Library/ABI version: major*10000 + minor*100 + patch. */
 int32_t gvr_version(void);
+
+/* Launch geometry of the two kernels on the current device (diagnostics): resident CTAs
+ * per SM, threads per CTA and dynamic shared memory per CTA.  Any pointer may be NULL.
+ * Returns GVR_ERR_CUDA if the occupancy query fails (no device). */
+gvr_status gvr_kernel_info(int32_t* gvr_ctas_per_sm, int32_t* gvr_threads, int32_t* gvr_smem_bytes,
+                           int32_t* radix_ctas_per_sm, int32_t* radix_threads, int32_t* radix_smem_bytes);
 
 #ifdef __cplusplus
 }

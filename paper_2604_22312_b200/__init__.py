@@ -65,8 +65,12 @@ def _load():
         fn.restype = ctypes.c_int
     lib.gvr_status_string.argtypes = [ctypes.c_int]
     lib.gvr_status_string.restype = ctypes.c_char_p
+    lib.gvr_last_cuda_error.argtypes = []
+    lib.gvr_last_cuda_error.restype = ctypes.c_char_p
     lib.gvr_version.argtypes = []
     lib.gvr_version.restype = ctypes.c_int32
+    lib.gvr_kernel_info.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 6
+    lib.gvr_kernel_info.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -76,9 +80,20 @@ def library():
     return _load()
 
 
+def kernel_info() -> dict:
+    """Resident CTAs per SM, threads and dynamic shared memory of both kernels (current device)."""
+    v = [ctypes.c_int32(0) for _ in range(6)]
+    _check(_load().gvr_kernel_info(*[ctypes.byref(x) for x in v]))
+    return {"gvr": {"ctas_per_sm": v[0].value, "threads": v[1].value, "smem_bytes": v[2].value},
+            "radix": {"ctas_per_sm": v[3].value, "threads": v[4].value, "smem_bytes": v[5].value}}
+
+
 def _check(rc: int):
     if rc != 0:
-        raise GvrError(_load().gvr_status_string(rc).decode())
+        msg = _load().gvr_status_string(rc).decode()
+        if rc == 3:
+            msg += ": " + _load().gvr_last_cuda_error().decode()
+        raise GvrError(msg)
 
 
 def _torch():

@@ -1,7 +1,8 @@
 // device_common.cuh — shared device building blocks of the GVR / radix Top-K kernels
-// (sm_100a): shared-memory layout, the sortable key transform, block reductions and
-// scans over 16 warps, the candidate-buffer count cache and in-place compaction, the
-// K-th-bin search, and the ordered-output stage.
+// (sm_100a): the sortable key transform, thread groups with their own named barrier
+// (a CTA may run several groups concurrently), group reductions and scans, the
+// candidate-buffer count cache and in-place compaction, the K-th-bin search, and the
+// ordered-output stage.
 //
 // PAPER.md references are to /root/reference/PAPER.md (arXiv 2604.22312).
 #pragma once
@@ -14,85 +15,18 @@
 namespace gvr {
 
 // ---------------------------------------------------------------------------------
-// Geometry and capacities.
-constexpr int NT = 256;                 // threads per CTA (the paper uses 512)
-constexpr int NW = NT / 32;             // 8 warps (the paper's K-th-bin search uses 16)
+// Constants.
 constexpr int KMAX = GVR_MAX_K;         // 2048
 constexpr int CWIN = GVR_WINDOW_C;      // Lemma-1 window upper bound C
-constexpr int CHUNK_SLOTS = 8;          // buffer slots per thread per compaction chunk
-constexpr int CHUNK = NT * CHUNK_SLOTS; // 2048 entries per chunk
-constexpr int NCHUNK = 4;
-constexpr int CAP = CHUNK * NCHUNK;     // 8192: capacity of the streamed candidate buffer B
 constexpr int NBINS = 2048;             // Phase-4 / radix histogram bins
+constexpr int CHUNK_SLOTS = 8;          // buffer slots per thread per compaction chunk
+constexpr int NCHUNK_MAX = 4;           // chunks per count cache (capacity <= 4 * 8 * group size)
 constexpr int VEC = 4;                  // float4 loads per thread per register tile
-constexpr int TILE_VEC = NT * VEC;      // float4s per register tile (8192 elements)
 constexpr int SORT_MAX = 4096;          // largest bitonic ordered-output sort (64-bit composites)
-constexpr int CSORT_MAX = 4096;         // largest counting-sort ordered output
 constexpr int CSORT_BIN_MAX = 32;       // counting sort: largest bin ranked in place
-constexpr int LIST_MAX = 4096;          // Phase 4: largest K-th-bin member list
+constexpr int LIST_MAX = 2048;          // Phase 4: largest K-th-bin member list
 constexpr int RADIX_EARLY = 2048;       // radix early exit
 constexpr unsigned FULL = 0xffffffffu;
-
-// TMA bulk-copy ring: NSTAGE stages of STAGE_FLOATS fp32 (16 per thread).
-constexpr int NSTAGE = 3;
-constexpr int STAGE_FLOATS = NT * 16;          // 4096
-constexpr int STAGE_BYTES = STAGE_FLOATS * 4;  // 16 KB
-
-static_assert(CAP >= CWIN, "buffer must hold the Lemma-1 window");
-static_assert(NBINS % NT == 0 && NBINS / NW % 32 == 0, "bin partitioning");
-static_assert(SORT_MAX <= CAP, "bitonic sort array aliases the buffer");
-
-// Shared-memory layout (dynamic): B = {bkey, bidx} is the candidate buffer (the 64-bit
-// bitonic sort array aliases it).  The TMA ring is idle once a row has been streamed
-// and then hosts the work area: histograms, the K-th-bin member list, counting sort.
-constexpr int OFF_BKEY = 0;
-constexpr int OFF_BIDX = OFF_BKEY + CAP * 4;
-constexpr int OFF_RING = OFF_BIDX + CAP * 4;               // 64 KB, 128-B aligned
-constexpr int OFF_WORK = OFF_RING;
-constexpr int OFF_HIST = OFF_WORK;                         // int32 [NBINS]     (ring alias)
-constexpr int OFF_AUX = OFF_WORK + NBINS * 4;              // int32 [NBINS]     (ring alias)
-constexpr int OFF_CSORT = OFF_WORK + 2 * NBINS * 4;        // u64 [CSORT_MAX]   (ring alias)
-constexpr int OFF_LIST = OFF_AUX;                          // u32 [LIST_MAX]    (Phase 4 only)
-constexpr int WORK_BYTES = 2 * NBINS * 4 + CSORT_MAX * 8;  // 48 KB
-constexpr int OFF_BAR = OFF_RING + NSTAGE * STAGE_BYTES;   // u64 [NSTAGE] mbarriers
-constexpr int OFF_RED = OFF_BAR + 64;                      // u32 [2][4][NW]
-constexpr int OFF_REDF = OFF_RED + 2 * 4 * NW * 4;         // f32 [2][2][NW]
-constexpr int OFF_MISC = OFF_REDF + 2 * 2 * NW * 4;        // int32 [32]
-constexpr int SMEM_BYTES = OFF_MISC + 32 * 4;              // 115,264 B -> 2 CTAs per SM
-static_assert(WORK_BYTES <= NSTAGE * STAGE_BYTES, "work area fits the idle ring");
-static_assert(OFF_LIST + LIST_MAX * 4 <= OFF_WORK + WORK_BYTES, "list fits the work area");
-static_assert(2 * (SMEM_BYTES + 1024) <= 233472, "two CTAs per SM");
-
-// Named barrier 1 over the CTA's NT threads.
-__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
-
-extern __shared__ __align__(128) unsigned char g_smem[];
-
-__device__ __forceinline__ uint32_t* s_bkey() { return reinterpret_cast<uint32_t*>(g_smem + OFF_BKEY); }
-__device__ __forceinline__ int32_t* s_bidx() { return reinterpret_cast<int32_t*>(g_smem + OFF_BIDX); }
-__device__ __forceinline__ unsigned long long* s_comp() { return reinterpret_cast<unsigned long long*>(g_smem + OFF_BKEY); }
-__device__ __forceinline__ int32_t* s_hist() { return reinterpret_cast<int32_t*>(g_smem + OFF_HIST); }
-__device__ __forceinline__ int32_t* s_aux() { return reinterpret_cast<int32_t*>(g_smem + OFF_AUX); }
-__device__ __forceinline__ unsigned long long* s_csort() { return reinterpret_cast<unsigned long long*>(g_smem + OFF_CSORT); }
-__device__ __forceinline__ uint32_t* s_list() { return reinterpret_cast<uint32_t*>(g_smem + OFF_LIST); }
-__device__ __forceinline__ float* s_ring() { return reinterpret_cast<float*>(g_smem + OFF_RING); }
-__device__ __forceinline__ uint32_t* s_red() { return reinterpret_cast<uint32_t*>(g_smem + OFF_RED); }
-__device__ __forceinline__ float* s_redf() { return reinterpret_cast<float*>(g_smem + OFF_REDF); }
-__device__ __forceinline__ int32_t* s_misc() { return reinterpret_cast<int32_t*>(g_smem + OFF_MISC); }
-
-struct Ctx {
-    int tid, lane, warp, par;
-};
-
-__device__ __forceinline__ Ctx make_ctx()
-{
-    Ctx c;
-    c.tid = threadIdx.x;
-    c.lane = threadIdx.x & 31;
-    c.warp = threadIdx.x >> 5;
-    c.par = 0;
-    return c;
-}
 
 // ---------------------------------------------------------------------------------
 // Sortable FP32 key: monotone uint32, negative -> flip all bits,
@@ -132,8 +66,68 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p)
 }
 
 // ---------------------------------------------------------------------------------
-// Block reductions.  Every call costs one csync(); scratch slots alternate
-// (c.par) so back-to-back calls need no second barrier.
+// A group of N threads (N/32 warps) synchronising on named barrier BAR.  Reductions
+// alternate between two scratch slots (par) so back-to-back calls need one barrier.
+constexpr int GROUP_SCRATCH_BYTES = 2 * 4 * 16 * 4 + 2 * 2 * 16 * 4 + 32 * 4;  // up to 16 warps
+
+template <int N_, int BAR_>
+struct Group {
+    static constexpr int N = N_;
+    static constexpr int W = N_ / 32;
+    static constexpr int BAR = BAR_;
+    static_assert(W <= 16 && N_ % 32 == 0, "group size");
+    int tid, lane, warp, par;
+    uint32_t* red;  // [2][4][W]
+    float* redf;    // [2][2][W]
+    int32_t* misc;  // [32]
+
+    __device__ __forceinline__ void init(int local_tid, unsigned char* scratch)
+    {
+        tid = local_tid;
+        lane = local_tid & 31;
+        warp = local_tid >> 5;
+        par = 0;
+        red = reinterpret_cast<uint32_t*>(scratch);
+        redf = reinterpret_cast<float*>(scratch + 2 * 4 * 16 * 4);
+        misc = reinterpret_cast<int32_t*>(scratch + 2 * 4 * 16 * 4 + 2 * 2 * 16 * 4);
+    }
+    __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(N) : "memory"); }
+    // barrier + group-wide OR of p in one instruction (BAR.RED.OR)
+    __device__ __forceinline__ bool sync_or(bool p) const
+    {
+        uint32_t r;
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbarrier.cta.red.or.pred q, %2, %3, p;\n\t"
+            "selp.u32 %0, 1, 0, q;\n\t}"
+            : "=r"(r)
+            : "r"((uint32_t)p), "n"(BAR), "n"(N)
+            : "memory");
+        return r != 0;
+    }
+};
+
+// Candidate buffer B: parallel key / index arrays of capacity cap.
+struct Buf {
+    uint32_t* key;
+    int32_t* idx;
+    int cap;
+    __device__ __forceinline__ unsigned long long* comp() const { return reinterpret_cast<unsigned long long*>(key); }
+};
+
+// Work area: NBINS-int histogram, NBINS-int aux (cursors / K-th-bin member list,
+// which may run on into csort), csort_cap composites for the counting sort.
+struct Work {
+    int32_t* hist;
+    int32_t* aux;
+    unsigned long long* csort;
+    int csort_cap;
+    __device__ __forceinline__ uint32_t* list() const { return reinterpret_cast<uint32_t*>(aux); }
+};
+__host__ __device__ constexpr int work_bytes(int csort_cap) { return 2 * NBINS * 4 + csort_cap * 8; }
+static_assert(LIST_MAX * 4 <= NBINS * 4 + KMAX * 8, "list fits aux + csort");
+
+// ---------------------------------------------------------------------------------
+// Group reductions.
 enum { R_ADD = 0, R_MIN = 1, R_MAX = 2 };
 
 template <int OP> __device__ __forceinline__ uint32_t wred(uint32_t v)
@@ -142,79 +136,77 @@ template <int OP> __device__ __forceinline__ uint32_t wred(uint32_t v)
     if (OP == R_MIN) return __reduce_min_sync(FULL, v);
     return __reduce_max_sync(FULL, v);
 }
-template <int OP> __device__ __forceinline__ uint32_t rident()
-{
-    return OP == R_MIN ? 0xffffffffu : 0u;
-}
+template <int OP> __device__ __forceinline__ uint32_t rident() { return OP == R_MIN ? 0xffffffffu : 0u; }
 
-template <int O0, int O1, int O2, int O3>
-__device__ __forceinline__ void block_red4(Ctx& c, uint32_t& a, uint32_t& b, uint32_t& d, uint32_t& e)
+template <int O0, int O1, int O2, int O3, class G>
+__device__ __forceinline__ void group_red4(G& c, uint32_t& a, uint32_t& b, uint32_t& d, uint32_t& e)
 {
     a = wred<O0>(a);
     b = wred<O1>(b);
     d = wred<O2>(d);
     e = wred<O3>(e);
-    uint32_t* s = s_red() + c.par * 4 * NW;
+    uint32_t* s = c.red + c.par * 4 * G::W;
     if (c.lane == 0) {
         s[c.warp] = a;
-        s[NW + c.warp] = b;
-        s[2 * NW + c.warp] = d;
-        s[3 * NW + c.warp] = e;
+        s[G::W + c.warp] = b;
+        s[2 * G::W + c.warp] = d;
+        s[3 * G::W + c.warp] = e;
     }
-    csync();
-    const bool in = c.lane < NW;
+    c.sync();
+    const bool in = c.lane < G::W;
     a = wred<O0>(in ? s[c.lane] : rident<O0>());
-    b = wred<O1>(in ? s[NW + c.lane] : rident<O1>());
-    d = wred<O2>(in ? s[2 * NW + c.lane] : rident<O2>());
-    e = wred<O3>(in ? s[3 * NW + c.lane] : rident<O3>());
+    b = wred<O1>(in ? s[G::W + c.lane] : rident<O1>());
+    d = wred<O2>(in ? s[2 * G::W + c.lane] : rident<O2>());
+    e = wred<O3>(in ? s[3 * G::W + c.lane] : rident<O3>());
     c.par ^= 1;
 }
 
-template <int O0, int O1>
-__device__ __forceinline__ void block_red2(Ctx& c, uint32_t& a, uint32_t& b)
+template <int O0, int O1, class G>
+__device__ __forceinline__ void group_red2(G& c, uint32_t& a, uint32_t& b)
 {
     a = wred<O0>(a);
     b = wred<O1>(b);
-    uint32_t* s = s_red() + c.par * 4 * NW;
+    uint32_t* s = c.red + c.par * 4 * G::W;
     if (c.lane == 0) {
         s[c.warp] = a;
-        s[NW + c.warp] = b;
+        s[G::W + c.warp] = b;
     }
-    csync();
-    const bool in = c.lane < NW;
+    c.sync();
+    const bool in = c.lane < G::W;
     a = wred<O0>(in ? s[c.lane] : rident<O0>());
-    b = wred<O1>(in ? s[NW + c.lane] : rident<O1>());
+    b = wred<O1>(in ? s[G::W + c.lane] : rident<O1>());
     c.par ^= 1;
 }
 
-template <int O0>
-__device__ __forceinline__ uint32_t block_red1(Ctx& c, uint32_t a)
+template <int O0, class G>
+__device__ __forceinline__ uint32_t group_red1(G& c, uint32_t a)
 {
     a = wred<O0>(a);
-    uint32_t* s = s_red() + c.par * 4 * NW;
+    uint32_t* s = c.red + c.par * 4 * G::W;
     if (c.lane == 0) s[c.warp] = a;
-    csync();
-    a = wred<O0>(c.lane < NW ? s[c.lane] : rident<O0>());
+    c.sync();
+    a = wred<O0>(c.lane < G::W ? s[c.lane] : rident<O0>());
     c.par ^= 1;
     return a;
 }
 
 // Deterministic fp32 sums of two channels (fixed shuffle tree + fixed warp order).
-__device__ __forceinline__ void block_fsum2(Ctx& c, float& a, float& b)
+template <class G>
+__device__ __forceinline__ void group_fsum2(G& c, float& a, float& b)
 {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(FULL, a, o);
         b += __shfl_xor_sync(FULL, b, o);
     }
-    float* s = s_redf() + c.par * 2 * NW;
+    float* s = c.redf + c.par * 2 * G::W;
     if (c.lane == 0) {
         s[c.warp] = a;
-        s[NW + c.warp] = b;
+        s[G::W + c.warp] = b;
     }
-    csync();
-    a = c.lane < NW ? s[c.lane] : 0.f;
-    b = c.lane < NW ? s[NW + c.lane] : 0.f;
+    c.sync();
+    a = c.lane < G::W ? s[c.lane] : 0.f;
+    b = c.lane < G::W ? s[G::W + c.lane] : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(FULL, a, o);
@@ -223,73 +215,76 @@ __device__ __forceinline__ void block_fsum2(Ctx& c, float& a, float& b)
     c.par ^= 1;
 }
 
-// Exclusive block scan of one u32 per thread (thread order); returns the thread's
-// offset and the block total.  Warp shuffles + one barrier: the ballot-free offset
-// computation of PAPER.md:600-604.
-__device__ __forceinline__ uint32_t block_excl_scan(Ctx& c, uint32_t v, uint32_t& total)
+// Inclusive warp scan (shuffles).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane)
 {
-    uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(FULL, x, o);
-        if (c.lane >= o) x += y;
+        const uint32_t y = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += y;
     }
-    uint32_t* s = s_red() + c.par * 4 * NW;
+    return v;
+}
+
+// Exclusive group scan of one u32 per thread (thread order); returns the thread's
+// offset and the total.  Warp shuffles + one barrier: the ballot-free offset
+// computation of PAPER.md:600-604.
+template <class G>
+__device__ __forceinline__ uint32_t group_excl_scan(G& c, uint32_t v, uint32_t& total)
+{
+    const uint32_t x = warp_incl_scan(v, c.lane);
+    uint32_t* s = c.red + c.par * 4 * G::W;
     if (c.lane == 31) s[c.warp] = x;
-    csync();
-    const uint32_t w = c.lane < NW ? s[c.lane] : 0u;
+    c.sync();
+    const uint32_t w = c.lane < G::W ? s[c.lane] : 0u;
     const uint32_t before = __reduce_add_sync(FULL, c.lane < c.warp ? w : 0u);
     total = __reduce_add_sync(FULL, w);
     c.par ^= 1;
     return before + x - v;
 }
 
-// Exclusive scan of v plus the block max of m, with one barrier.
-__device__ __forceinline__ uint32_t block_excl_scan_max(Ctx& c, uint32_t v, uint32_t m, uint32_t& total,
-                                                        uint32_t& mall)
+// Exclusive scan of v plus the group max of m, with one barrier.
+template <class G>
+__device__ __forceinline__ uint32_t group_excl_scan_max(G& c, uint32_t v, uint32_t m, uint32_t& total, uint32_t& mall)
 {
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(FULL, x, o);
-        if (c.lane >= o) x += y;
-    }
+    const uint32_t x = warp_incl_scan(v, c.lane);
     const uint32_t wm = __reduce_max_sync(FULL, m);
-    uint32_t* s = s_red() + c.par * 4 * NW;
+    uint32_t* s = c.red + c.par * 4 * G::W;
     if (c.lane == 31) {
         s[c.warp] = x;
-        s[NW + c.warp] = wm;
+        s[G::W + c.warp] = wm;
     }
-    __syncwarp();
-    csync();
-    const uint32_t w = c.lane < NW ? s[c.lane] : 0u;
+    c.sync();
+    const uint32_t w = c.lane < G::W ? s[c.lane] : 0u;
     const uint32_t before = __reduce_add_sync(FULL, c.lane < c.warp ? w : 0u);
     total = __reduce_add_sync(FULL, w);
-    mall = __reduce_max_sync(FULL, c.lane < NW ? s[NW + c.lane] : 0u);
+    mall = __reduce_max_sync(FULL, c.lane < G::W ? s[G::W + c.lane] : 0u);
     c.par ^= 1;
     return before + x - v;
 }
 
 // ---------------------------------------------------------------------------------
-// Candidate buffer B: slot p of chunk ch for thread t is ch*CHUNK + j*NT + t.  Counting
-// passes cache per-chunk counts (the "count cache" of PAPER.md:588-597, applied to the
-// shared-memory buffer) so that the following compaction needs no recount.
+// Count cache over B (the "count cache" of PAPER.md:588-597, applied to the shared-
+// memory buffer): slot p of chunk ch for thread t is ch*CHUNK + j*N + t with
+// CHUNK = 8*N; per-chunk counts of the last count pass let the following compaction
+// skip the recount.
 struct ChunkCounts {
-    uint32_t c[NCHUNK];
+    uint32_t c[NCHUNK_MAX];
 };
 
-__device__ __forceinline__ ChunkCounts count_chunks_ge(const Ctx& c, int fill, uint32_t T)
+template <class G>
+__device__ __forceinline__ ChunkCounts count_chunks_ge(const G& c, const Buf& B, int fill, uint32_t T)
 {
-    const uint32_t* bkey = s_bkey();
+    constexpr int CHUNK = G::N * CHUNK_SLOTS;
     ChunkCounts cc;
 #pragma unroll
-    for (int ch = 0; ch < NCHUNK; ++ch) {
+    for (int ch = 0; ch < NCHUNK_MAX; ++ch) {
         uint32_t n = 0;
-        if (ch * CHUNK < fill) {  // block-uniform: skip empty chunks
+        if (ch * CHUNK < fill) {  // group-uniform: skip empty chunks
 #pragma unroll
             for (int j = 0; j < CHUNK_SLOTS; ++j) {
-                const int p = ch * CHUNK + j * NT + c.tid;
-                if (p < fill && bkey[p] >= T) ++n;
+                const int p = ch * CHUNK + j * G::N + c.tid;
+                if (p < fill && B.key[p] >= T) ++n;
             }
         }
         cc.c[ch] = n;
@@ -301,7 +296,7 @@ __device__ __forceinline__ uint32_t chunk_total(const ChunkCounts& cc)
 {
     uint32_t s = 0;
 #pragma unroll
-    for (int ch = 0; ch < NCHUNK; ++ch) s += cc.c[ch];
+    for (int ch = 0; ch < NCHUNK_MAX; ++ch) s += cc.c[ch];
     return s;
 }
 
@@ -309,76 +304,67 @@ __device__ __forceinline__ uint32_t chunk_total(const ChunkCounts& cc)
 // the cached per-chunk counts of the last count pass at T.  Chunk ch writes only to
 // positions below (ch+1)*CHUNK, and every thread has loaded its chunk-ch slots before
 // the scan barrier, so no slot is overwritten before it is read.  Returns new fill.
-__device__ __forceinline__ int compact_ge(Ctx& c, int fill, uint32_t T, const ChunkCounts& cc)
+template <class G>
+__device__ __forceinline__ int compact_ge(G& c, const Buf& B, int fill, uint32_t T, const ChunkCounts& cc)
 {
-    uint32_t* bkey = s_bkey();
-    int32_t* bidx = s_bidx();
+    constexpr int CHUNK = G::N * CHUNK_SLOTS;
     int out_base = 0;
 #pragma unroll
-    for (int ch = 0; ch < NCHUNK; ++ch) {
-        if (ch * CHUNK >= fill) break;  // block-uniform
+    for (int ch = 0; ch < NCHUNK_MAX; ++ch) {
+        if (ch * CHUNK >= fill) break;  // group-uniform
         uint32_t kk[CHUNK_SLOTS];
         int32_t ii[CHUNK_SLOTS];
 #pragma unroll
         for (int j = 0; j < CHUNK_SLOTS; ++j) {
-            const int p = ch * CHUNK + j * NT + c.tid;
+            const int p = ch * CHUNK + j * G::N + c.tid;
             kk[j] = 0u;
             ii[j] = 0;
             if (p < fill) {
-                kk[j] = bkey[p];
-                ii[j] = bidx[p];
+                kk[j] = B.key[p];
+                ii[j] = B.idx[p];
             }
         }
         uint32_t tot;
-        int pos = out_base + (int)block_excl_scan(c, cc.c[ch], tot);
+        int pos = out_base + (int)group_excl_scan(c, cc.c[ch], tot);
 #pragma unroll
         for (int j = 0; j < CHUNK_SLOTS; ++j) {
-            const int p = ch * CHUNK + j * NT + c.tid;
+            const int p = ch * CHUNK + j * G::N + c.tid;
             if (p < fill && kk[j] >= T) {
-                bkey[pos] = kk[j];
-                bidx[pos] = ii[j];
+                B.key[pos] = kk[j];
+                B.idx[pos] = ii[j];
                 ++pos;
             }
         }
         out_base += (int)tot;
     }
-    csync();
+    c.sync();
     return out_base;
-}
-
-// Max key over B[0, fill) (thread-local part).
-__device__ __forceinline__ uint32_t buffer_max_local(const Ctx& c, int fill)
-{
-    const uint32_t* bkey = s_bkey();
-    uint32_t m = 0;
-    for (int p = c.tid; p < fill; p += NT) m = max(m, bkey[p]);
-    return m;
 }
 
 // ---------------------------------------------------------------------------------
 // K-th bin search: find bin b with
 //   sum(hist[b+1..nb)) < krem <= sum(hist[b..nb)).
-// Each warp owns nb/NW consecutive bins, warp totals are combined from the top, the
+// Each warp owns nb/W consecutive bins, warp totals are combined from the top, the
 // owning lane resolves the exact bin.  Requires 1 <= krem <= sum(hist).
-__device__ __forceinline__ void kth_bin(Ctx& c, int nb, uint32_t krem, int& b_out, uint32_t& above_out)
+template <class G>
+__device__ __forceinline__ void kth_bin(G& c, const int32_t* hist, int nb, uint32_t krem, int& b_out,
+                                        uint32_t& above_out)
 {
-    const int32_t* hist = s_hist();
-    int32_t* misc = s_misc();
-    const int per = nb / NW;  // 128 or 64
-    const int q = per / 32;   // 4 or 2
+    const int per = nb / G::W;
+    const int q = per / 32;
     const int base = c.warp * per + c.lane * q;
     uint32_t ls = 0;
     for (int i = 0; i < q; ++i) ls += (uint32_t)hist[base + i];
     const uint32_t wt = __reduce_add_sync(FULL, ls);
-    uint32_t* s = s_red() + c.par * 4 * NW;
+    uint32_t* s = c.red + c.par * 4 * G::W;
     if (c.lane == 0) s[c.warp] = wt;
-    csync();
-    const uint32_t v = c.lane < NW ? s[c.lane] : 0u;
-    const uint32_t above_w = __reduce_add_sync(FULL, (c.lane > c.warp && c.lane < NW) ? v : 0u);
+    c.sync();
+    const uint32_t v = c.lane < G::W ? s[c.lane] : 0u;
+    const uint32_t above_w = __reduce_add_sync(FULL, (c.lane > c.warp && c.lane < G::W) ? v : 0u);
     uint32_t x = ls;  // inclusive suffix over lanes
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_down_sync(FULL, x, o);
+        const uint32_t y = __shfl_down_sync(FULL, x, o);
         if (c.lane + o < 32) x += y;
     }
     const uint32_t above_g = above_w + x - ls;
@@ -387,83 +373,35 @@ __device__ __forceinline__ void kth_bin(Ctx& c, int nb, uint32_t krem, int& b_ou
         for (int i = q - 1; i >= 0; --i) {
             const uint32_t h = (uint32_t)hist[base + i];
             if (a + h >= krem) {
-                misc[0] = base + i;
-                misc[1] = (int32_t)a;
+                c.misc[0] = base + i;
+                c.misc[1] = (int32_t)a;
                 break;
             }
             a += h;
         }
     }
-    csync();
-    b_out = misc[0];
-    above_out = (uint32_t)misc[1];
+    c.sync();
+    b_out = c.misc[0];
+    above_out = (uint32_t)c.misc[1];
     c.par ^= 1;
-    csync();  // misc may be reused immediately
+    c.sync();  // misc may be reused immediately
 }
 
-__device__ __forceinline__ void zero_hist(const Ctx& c, int32_t* h, int nb)
+template <class G>
+__device__ __forceinline__ void zero_ints(const G& c, int32_t* h, int nb)
 {
-    for (int i = c.tid; i < nb; i += NT) h[i] = 0;
+    for (int i = c.tid; i < nb; i += G::N) h[i] = 0;
 }
 
 // Smallest s with (width - 1) >> s < NBINS (width in [1, 2^32]).
 __device__ __forceinline__ int shift_for_width(uint64_t width)
 {
     const uint32_t w = (uint32_t)(width - 1ull);
-    const int bits = 32 - __clz(w);  // bits needed for w
+    const int bits = 32 - __clz(w);
     return bits > 11 ? bits - 11 : 0;
 }
 
-// ---------------------------------------------------------------------------------
-// Ordered output (not part of the paper, whose output is an unordered partition with
-// non-deterministic ties, PAPER.md:647-648, 849-851): the selected entries are sorted by
-// the 64-bit composite (key << 32 | ~idx) descending = (score desc, index asc).
-
-// Bitonic fallback: P (power of two, <= SORT_MAX) composites in the aliasing array.
-__device__ __forceinline__ void bitonic_sort_desc(Ctx& c, int P)
-{
-    unsigned long long* a = s_comp();
-    for (int kk = 2; kk <= P; kk <<= 1) {
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-            for (int i = c.tid; i < (P >> 1); i += NT) {
-                const int lo = 2 * i - (i & (j - 1));
-                const int hi = lo + j;
-                const bool desc = (lo & kk) == 0;
-                const unsigned long long A = a[lo], B = a[hi];
-                if ((A < B) == desc) {
-                    a[lo] = B;
-                    a[hi] = A;
-                }
-            }
-            csync();
-        }
-    }
-}
-
-__device__ __forceinline__ int pow2_at_least(int m)
-{
-    int p = 64;
-    while (p < m) p <<= 1;
-    return p;
-}
-
-__device__ __forceinline__ void write_output(const Ctx& c, const unsigned long long* sorted, int take, int k,
-                                             int32_t* out, float* out_val)
-{
-    for (int j = c.tid; j < k; j += NT) {
-        int32_t idx = -1;
-        float val = 0.f;
-        if (j < take) {
-            const unsigned long long cv = sorted[j];
-            idx = comp_idx(cv);
-            val = key2f(comp_key(cv));
-        }
-        out[j] = idx;
-        if (out_val) out_val[j] = val;
-    }
-}
-
-// Linear bin of d = key - Tsel over [0, range) with all NBINS bins in use:
+// Linear bin of d = key - lo over [0, range) using all NBINS bins:
 // (d * scale) >> 32 with scale = floor(2^32 * NBINS / range), monotone in d.
 __device__ __forceinline__ uint32_t bin_scale(uint64_t range)
 {
@@ -475,40 +413,73 @@ __device__ __forceinline__ int lin_bin(uint32_t d, uint32_t scale)
     return min((int)(((uint64_t)d * scale) >> 32), NBINS - 1);
 }
 
+// ---------------------------------------------------------------------------------
+// Ordered output (not part of the paper, whose output is an unordered partition with
+// non-deterministic ties, PAPER.md:647-648, 849-851): the selected entries are sorted by
+// the 64-bit composite (key << 32 | ~idx) descending = (score desc, index asc).
+
+// Bitonic fallback: P (power of two, <= SORT_MAX) composites in the aliasing array.
+template <class G>
+__device__ __forceinline__ void bitonic_sort_desc(G& c, unsigned long long* a, int P)
+{
+    for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = c.tid; i < (P >> 1); i += G::N) {
+                const int lo = 2 * i - (i & (j - 1));
+                const int hi = lo + j;
+                const bool desc = (lo & kk) == 0;
+                const unsigned long long A = a[lo], Bv = a[hi];
+                if ((A < Bv) == desc) {
+                    a[lo] = Bv;
+                    a[hi] = A;
+                }
+            }
+            c.sync();
+        }
+    }
+}
+
+__device__ __forceinline__ int pow2_at_least(int m)
+{
+    int p = 64;
+    while (p < m) p <<= 1;
+    return p;
+}
+
 // Emit the entries of B[0, fill) with key >= Tsel (n_sel of them, n_sel <= SORT_MAX),
 // sorted, as the row's first `take` outputs, then -1 padding up to k.
-// Counting sort: a 2048-bin linear histogram over [Tsel, kmax] (bin 0 = highest keys), bin
-// offsets by one block scan, scatter with per-bin cursors, then every entry is ranked
-// among the (few) entries that share its bin, in parallel.  Falls back to the bitonic sort when the
-// selection or a bin is too large.
-__device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uint32_t kmax_sel, int n_sel, int take,
-                                            int k, int32_t* out, float* out_val)
+// Counting sort: a 2048-bin linear histogram over [Tsel, kmax] (bin 0 = highest keys),
+// bin offsets by one group scan, scatter with per-bin cursors, then every entry is
+// ranked among the (few) entries that share its bin, in parallel.  Falls back to the
+// bitonic sort (in B's memory) when the selection or a bin is too large.
+// kmax_sel = 0 means "unknown" (computed here).
+template <class G>
+__device__ __forceinline__ void emit_sorted(G& c, const Buf& B, const Work& Wk, int fill, uint32_t Tsel,
+                                            uint32_t kmax_sel, int n_sel, int take, int k, int32_t* out,
+                                            float* out_val)
 {
-    uint32_t* bkey = s_bkey();
-    int32_t* bidx = s_bidx();
-    int32_t* hist = s_hist();
-    int32_t* cur = s_aux();
-    zero_hist(c, hist, NBINS);
+    int32_t* hist = Wk.hist;
+    int32_t* cur = Wk.aux;
+    zero_ints(c, hist, NBINS);
     uint32_t kmx = kmax_sel;
-    if (kmx == 0u) {  // not known by the caller
-        for (int p = c.tid; p < fill; p += NT) {
-            const uint32_t kv = bkey[p];
+    if (kmx == 0u) {
+        for (int p = c.tid; p < fill; p += G::N) {
+            const uint32_t kv = B.key[p];
             if (kv >= Tsel) kmx = max(kmx, kv);
         }
-        kmx = block_red1<R_MAX>(c, kmx);  // (barrier also orders the zeroing)
+        kmx = group_red1<R_MAX>(c, kmx);  // (barrier also orders the zeroing)
     } else {
-        csync();
+        c.sync();
     }
     const uint32_t scale = bin_scale((uint64_t)kmx - Tsel + 1ull);
-    bool counting = n_sel <= CSORT_MAX;
+    bool counting = n_sel <= Wk.csort_cap;
     if (counting) {
-        for (int p = c.tid; p < fill; p += NT) {
-            const uint32_t kv = bkey[p];
+        for (int p = c.tid; p < fill; p += G::N) {
+            const uint32_t kv = B.key[p];
             if (kv >= Tsel) atomicAdd(&hist[(NBINS - 1) - lin_bin(kv - Tsel, scale)], 1);
         }
-        csync();
-        // exclusive scan over bins (BPT consecutive bins per thread)
-        constexpr int BPT = NBINS / NT;
+        c.sync();
+        constexpr int BPT = NBINS / G::N;  // consecutive bins per thread
         const int b0 = c.tid * BPT;
         int h[BPT];
         uint32_t loc = 0, mx = 0;
@@ -519,7 +490,7 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
             mx = max(mx, (uint32_t)h[i]);
         }
         uint32_t tot;
-        uint32_t off = block_excl_scan_max(c, loc, mx, tot, mx);
+        uint32_t off = group_excl_scan_max(c, loc, mx, tot, mx);
         counting = mx <= (uint32_t)CSORT_BIN_MAX;
         if (counting) {
 #pragma unroll
@@ -527,22 +498,22 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
                 cur[b0 + i] = (int)off;  // bin start; becomes the bin end after the scatter
                 off += (uint32_t)h[i];
             }
-            csync();
-            unsigned long long* cs = s_csort();
-            for (int p = c.tid; p < fill; p += NT) {
-                const uint32_t kv = bkey[p];
+            c.sync();
+            unsigned long long* cs = Wk.csort;
+            for (int p = c.tid; p < fill; p += G::N) {
+                const uint32_t kv = B.key[p];
                 if (kv >= Tsel) {
                     const int b = (NBINS - 1) - lin_bin(kv - Tsel, scale);
                     const int slot = atomicAdd(&cur[b], 1);
-                    cs[slot] = make_comp(kv, bidx[p]);
+                    cs[slot] = make_comp(kv, B.idx[p]);
                 }
             }
-            csync();
-            // rank every entry inside its (small) bin in parallel: final position =
-            // bin start + #entries of the bin with a larger composite; B is free now
-            int32_t* fidx = s_bidx();
-            float* fval = reinterpret_cast<float*>(s_bkey());
-            for (int j = c.tid; j < n_sel; j += NT) {
+            c.sync();
+            // rank every entry inside its (small) bin in parallel: final position = bin
+            // start + #entries of the bin with a larger composite; B is free now
+            int32_t* fidx = B.idx;
+            float* fval = reinterpret_cast<float*>(B.key);
+            for (int j = c.tid; j < n_sel; j += G::N) {
                 const unsigned long long v = cs[j];
                 const int b = (NBINS - 1) - lin_bin(comp_key(v) - Tsel, scale);
                 const int cnt = hist[b];
@@ -555,38 +526,48 @@ __device__ __forceinline__ void emit_sorted(Ctx& c, int fill, uint32_t Tsel, uin
                     fval[pos] = key2f(comp_key(v));
                 }
             }
-            csync();
-            for (int j = c.tid; j < k; j += NT) {
+            c.sync();
+            for (int j = c.tid; j < k; j += G::N) {
                 const bool in = j < take;
                 out[j] = in ? fidx[j] : -1;
                 if (out_val) out_val[j] = in ? fval[j] : 0.f;
             }
+            c.sync();  // B is reused by the caller
             return;
         }
     }
-    // bitonic fallback: gather the selection into the aliasing composite array
-    constexpr int PER = SORT_MAX / NT;  // 16
+    // bitonic fallback: compact the selection, then sort composites in B's memory
+    constexpr int PER = SORT_MAX / G::N;
     unsigned long long v[PER];
-    // compact the selected entries of this thread's slots first (order-free)
-    ChunkCounts cc = count_chunks_ge(c, fill, Tsel);
-    const int m = compact_ge(c, fill, Tsel, cc);
+    ChunkCounts cc = count_chunks_ge(c, B, fill, Tsel);
+    const int m = compact_ge(c, B, fill, Tsel, cc);
     const int P = pow2_at_least(m);
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        const int p = j * NT + c.tid;
+        const int p = j * G::N + c.tid;
         v[j] = 0ull;
-        if (p < m) v[j] = make_comp(bkey[p], bidx[p]);
+        if (p < m) v[j] = make_comp(B.key[p], B.idx[p]);
     }
-    csync();  // all reads of B done before the aliasing writes
-    unsigned long long* comp = s_comp();
+    c.sync();  // all reads of B done before the aliasing writes
+    unsigned long long* comp = B.comp();
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        const int p = j * NT + c.tid;
+        const int p = j * G::N + c.tid;
         if (p < P) comp[p] = v[j];
     }
-    csync();
-    bitonic_sort_desc(c, P);
-    write_output(c, comp, take, k, out, out_val);
+    c.sync();
+    bitonic_sort_desc(c, comp, P);
+    for (int j = c.tid; j < k; j += G::N) {
+        int32_t idx = -1;
+        float val = 0.f;
+        if (j < take) {
+            idx = comp_idx(comp[j]);
+            val = key2f(comp_key(comp[j]));
+        }
+        out[j] = idx;
+        if (out_val) out_val[j] = val;
+    }
+    c.sync();
 }
 
 }  // namespace gvr

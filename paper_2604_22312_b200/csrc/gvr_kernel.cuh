@@ -1,18 +1,19 @@
-// gvr_kernel.cuh — Guess-Verify-Refine exact Top-K on sm_100a: one 256-thread CTA per
-// row, two CTAs per SM (one streams while the other refines), TMA bulk-copy ring.
+// gvr_kernel.cuh — Guess-Verify-Refine exact Top-K on sm_100a.
 //
-// Method: PAPER.md Sec. 4 (lines 379-690).  Per row, as executed here:
+// One CTA of 256 threads per row, two CTAs per SM (115.6 KB of shared memory each), so
+// one CTA streams while the other evaluates its guess or refines.
+//
+// Method: PAPER.md Sec. 4 (lines 379-690).  Per row:
 //   Phase 1 (Guess): x at the previous step's Top-K positions ->
-//     pmin / pmax / pmean (Eq. 4) plus the second moment (the first ring tiles are
-//     already in flight).
+//     pmin / pmax / pmean (Eq. 4) plus the second moment; T_c = pmean - sigma*sd.  The
+//     TMA ring is primed first, so the first 64 KB of the row load during Phase 1.
 //   Streaming pass (B200 re-design of the Phase-2 count pass fused with the Phase-3
-//     collector): the row body is read from HBM exactly once by TMA
-//     bulk copies into a 3 x 16 KB shared-memory ring (pipeline.cuh); every thread
-//     appends its elements (16 per tile) whose key is >= the collect
-//     threshold T_c to the candidate buffer B in shared memory (ballot-free, block-scan
-//     offsets).  B holds {x >= T_c}, so f(T) for every T >= T_c is counted from B alone
-//     (Lemma 1).  If B would overflow, T_c is raised by a secant
-//     search over B (Eq. 6) to a threshold that still keeps >= K elements.
+//     collector): the row body is read from HBM exactly once, in
+//     rounds of 2 x 16 KB TMA tiles; every element whose key is >= T_c is appended to
+//     B (warp scan + one shared atomic per warp: ballot-free).
+//     B holds {x >= T_c}, so f(T) for every T >= T_c is counted from B alone (Lemma 1,
+//     PAPER.md:401-415).  If B would overflow, T_c is raised by a secant search over B
+//     (Eq. 6) to a threshold that still keeps >= K elements.
 //   Phase 2: secant search of Eq. 6 toward f_target inside the
 //     window K <= f(T) <= C, starting from T0 = pmean, with first-step damping and
 //     bisection fallback — counts from B (shared memory), not from HBM.
@@ -25,9 +26,10 @@
 //     all candidates); exact narrowing of the bin if it is too large.
 //   Ordered output: candidates >= T* sorted by (key desc, index asc), first K written.
 //   Fallbacks (R12/R13): massive ties or an
-//     underflowing guess (f(T_c) < K) -> exact radix select + ordered tie fill from
+//     overshooting guess (f(T_c) < K) -> exact radix select + ordered tie fill from
 //     global memory.
 #pragma once
+#include "pipeline.cuh"
 #include "select_global.cuh"
 
 namespace gvr {
@@ -37,8 +39,41 @@ struct GvrParams {
     int max_secant;
 };
 
-struct RowStats {
-    int secant, snap, cand, done, passes, raises, bufcnt;
+constexpr int GVR_NT = 256;
+constexpr int GVR_CAP = 6016;   // candidate buffer capacity (C = 6144 less the raise histogram)
+constexpr int RAISE_BINS = 256;  // raise_threshold histogram (one bin per thread)
+constexpr int GVR_CSORT = KMAX;  // counting-sort capacity
+using GvrGroup = Group<GVR_NT, 1>;
+
+// Shared-memory layout (dynamic).  The refine work area aliases the ring, which is idle
+// once the stream is done.
+constexpr int G_OFF_RING = 0;
+constexpr int G_OFF_B = G_OFF_RING + NSTAGE * STAGE_BYTES;  // {key[CAP], idx[CAP]}
+constexpr int G_OFF_WORK = G_OFF_RING;
+constexpr int G_OFF_RHIST = G_OFF_B + GVR_CAP * 8;          // raise histogram [RAISE_BINS]
+constexpr int G_OFF_BARS = G_OFF_RHIST + RAISE_BINS * 4;    // full[NSTAGE]
+constexpr int G_OFF_SCR = G_OFF_BARS + NSTAGE * 8;
+constexpr int GVR_SMEM_BYTES = G_OFF_SCR + GROUP_SCRATCH_BYTES;
+static_assert(work_bytes(GVR_CSORT) <= NSTAGE * STAGE_BYTES, "work area fits in the ring");
+static_assert(GVR_SMEM_BYTES + 1024 <= 233472 / 2, "two CTAs per SM");
+static_assert(GVR_CAP >= 2 * KMAX && GVR_CAP <= NCHUNK_MAX * CHUNK_SLOTS * GVR_NT, "buffer capacity");
+static_assert(GVR_CAP * 8 >= SORT_MAX * 8, "bitonic fallback aliases the buffer");
+static_assert(ROUND_FLOATS == 32 * GVR_NT, "32 elements per thread per round");
+static_assert(RAISE_BINS == GVR_NT, "one raise bin per thread");
+
+// Phase timestamps (written when phase_ts != nullptr): the paper's GVR_PHASE_TIMING
+// instrumentation.
+enum { TS_START = 0, TS_PHASE1, TS_STREAM, TS_PHASE23, TS_PHASE4, TS_END, TS_N };
+
+// What the streaming pass hands to Phases 2-4.
+struct RowMeta {
+    int fill;         // entries in B
+    uint32_t Tc;      // collect threshold (after raises)
+    uint32_t ftc;     // f(T_c) = fill - extras
+    uint32_t kmax;    // max key in B
+    uint32_t extras;  // superset entries (NaN / -0 against +0) with key < T_c
+    uint32_t T0;      // f2key(pmean)
+    bool t0_ok;
 };
 
 // Secant step of Eq. 6 in value space between the anchors
@@ -64,370 +99,485 @@ __device__ __forceinline__ uint32_t secant_step(uint64_t lo, uint32_t clo, uint6
     return (uint32_t)(lo + ((hi - lo) >> 1));
 }
 
-// Element e (0..15) of a consumer thread's share of a ring tile sits at stage float
-// 4*(tid + (e>>2)*NT) + (e&3): float4 j = e>>2 of the thread is vector tid + j*NT.
-__device__ __forceinline__ int tile_pos(int tid, int e) { return 4 * (tid + (e >> 2) * NT) + (e & 3); }
 
-// Raise the collect threshold when B would overflow.  B[0, fill) and
-// the tile's elements >= Tc together exceed CAP.  Find T > Tc whose count over B plus
-// the tile lies in [K, CAP/2] by Eq. 6 secant steps aimed at K <= f_target*phi <= CAP/2
-// (phi = streamed fraction of the row), compact B to {key >= T} and return 0; return 1
-// if no such T exists (massive ties).  The tile is re-read from the ring stage.
-__device__ __noinline__ int raise_threshold(const float* sp, uint32_t vmask, uint32_t& Tc, int& fill,
-                                            uint32_t c_at_tc, float phi, int K, int max_secant, int& raises,
-                                            int& par)
+// Round geometry: warp w owns floats [1024 w, 1024 (w+1)) of the 8192-float round
+// block; lane l's float4 j (0..7) is at 1024 w + 128 j + 4 l, so every warp load is 512
+// contiguous bytes (conflict-free).  Element e = 4 j + c of the 32-bit pass mask sits at
+// lane_base + rel_off(e).
+__device__ __forceinline__ int lane_base(int warp, int lane) { return 1024 * warp + 4 * lane; }
+__device__ __forceinline__ int rel_off(int e) { return ((e & ~3) << 5) | (e & 3); }
+
+// Raise the collect threshold when B would overflow.  Called by the
+// whole group after a round in which some warps could not reserve space: B[0, fill)
+// plus the round elements held by those warps (held mask, elements at sp[lb +
+// rel_off(e)]) exceed the capacity.  Finds a key T > Tc whose count over B and the held
+// elements lies in [K, cap/2], as close as possible to f_target*phi (phi = streamed
+// fraction of the row, so the count extrapolates to f_target at the row's end), by a
+// key-space radix search: a 256-bin histogram of [base, base + width) per level, suffix
+// counts at the bin edges, then either an acceptable edge or narrowing into the bin
+// where the count crosses K.  Compacts B to {key >= T} and returns 0, or returns 1 if
+// no such T exists (massive ties).  mx = max key over B and the held elements.
+__device__ __noinline__ int raise_threshold(GvrGroup& c, const Buf& B, int32_t* hist, const float* sp, int lb,
+                                            uint32_t held, uint32_t& Tc, int& fill, uint32_t mx, float phi, int K,
+                                            int& raises)
 {
-    Ctx c = make_ctx();
-    c.par = par;
-    uint32_t mx = buffer_max_local(c, fill);
-    for (int e = 0; e < 16; ++e)
-        if ((vmask >> e) & 1u) mx = max(mx, f2key(sp[tile_pos(c.tid, e)]));
-    mx = block_red1<R_MAX>(c, mx);
-    uint64_t lo = Tc, hi = (uint64_t)mx + 1ull;  // exclusive upper anchor
-    uint32_t clo = c_at_tc, chi = 0;
-    const uint32_t acc_hi = CAP / 2;
+    const uint32_t acc_hi = (uint32_t)B.cap / 2;
     const float ft = 0.5f * (float)(K + CWIN);
-    const float target = fminf(fmaxf(ft * phi, (float)K), (float)acc_hi);
-    uint32_t T = Tc;
-    ChunkCounts cc;
-    int rc = 0;
-    for (int it = 0;; ++it) {
-        if (it >= 64) {  // safety bound (bisection needs <= 32 steps)
-            rc = 1;
+    const uint32_t target = (uint32_t)fminf(fmaxf(ft * phi, (float)K), (float)acc_hi);
+    uint32_t base = Tc, above = 0;
+    uint64_t width = (uint64_t)mx - Tc + 1ull;
+    uint32_t T = 0;
+    int rc = 1;
+    for (int level = 0; level < 5; ++level) {
+        const int s = width > (uint64_t)RAISE_BINS ? 64 - __clzll((long long)(width - 1)) - 8 : 0;
+        hist[c.tid] = 0;
+        c.sync();
+        for (int p = c.tid; p < fill; p += GVR_NT) {
+            const uint32_t kk = B.key[p];
+            if (kk >= base && (uint64_t)(kk - base) < width) atomicAdd(&hist[(kk - base) >> s], 1);
+        }
+        for (uint32_t m = held; m; m &= m - 1) {
+            const uint32_t kk = f2key(sp[lb + rel_off(__ffs(m) - 1)]);
+            if (kk >= base && (uint64_t)(kk - base) < width) atomicAdd(&hist[(kk - base) >> s], 1);
+        }
+        c.sync();
+        // thread t owns bin b = 255 - t: S_b = count(key >= edge(b)) = above + sum_{b' >= b} hist
+        const int b = RAISE_BINS - 1 - c.tid;
+        const uint32_t h = (uint32_t)hist[b];
+        uint32_t tot;
+        const uint32_t Sb = above + group_excl_scan(c, h, tot) + h;
+        // edges with S >= target / S >= K form prefixes [0, m) of the bins
+        uint32_t m_t = Sb >= target ? 1u : 0u, m_k = Sb >= (uint32_t)K ? 1u : 0u;
+        group_red2<R_ADD, R_ADD>(c, m_t, m_k);
+        const int bt = (int)m_t - 1, bk = (int)m_k - 1;
+        if (b == bt) c.misc[20] = (int)Sb;
+        if (b == bk) c.misc[21] = (int)Sb;
+        if (b == bk + 1) c.misc[22] = (int)Sb;
+        c.sync();
+        const uint32_t St = bt >= 0 ? (uint32_t)c.misc[20] : 0u;
+        const uint32_t Sk = (uint32_t)c.misc[21];
+        const uint32_t Snext = bk + 1 < RAISE_BINS ? (uint32_t)c.misc[22] : above;
+        c.sync();
+        if (bk < 0) break;  // cannot happen: S at the lowest edge is >= K
+        if (bt >= 0 && St <= acc_hi) {
+            T = base + ((uint32_t)bt << s);
+            rc = 0;
             break;
         }
-        if (hi - lo < 2) {
-            // adjacent keys: no threshold in [K, CAP/2]; lo still fits if clo <= CAP
-            if (clo > (uint32_t)CAP || lo == (uint64_t)Tc) {
-                rc = 1;
-                break;
+        if (Sk <= acc_hi) {
+            T = base + ((uint32_t)bk << s);
+            rc = 0;
+            break;
+        }
+        if (s == 0) {  // one key value holds the crossing: keep it if B can hold it
+            if (Sk <= (uint32_t)B.cap && base + (uint32_t)bk != Tc) {
+                T = base + (uint32_t)bk;
+                rc = 0;
             }
-            T = (uint32_t)lo;
-            cc = count_chunks_ge(c, fill, T);
             break;
         }
-        T = secant_step(lo, clo, hi, chi, target, it == 0, it >= max_secant);
-        cc = count_chunks_ge(c, fill, T);
-        uint32_t cnt = chunk_total(cc);
-        for (int e = 0; e < 16; ++e)
-            if (((vmask >> e) & 1u) && f2key(sp[tile_pos(c.tid, e)]) >= T) ++cnt;
-        cnt = block_red1<R_ADD>(c, cnt);
-        if (cnt >= (uint32_t)K && cnt <= acc_hi) break;
-        if (cnt > acc_hi) {
-            lo = T;
-            clo = cnt;
-        } else {
-            hi = T;
-            chi = cnt;
-        }
+        base += (uint32_t)bk << s;
+        width = 1ull << s;
+        above = Snext;
     }
     if (rc == 0) {
-        fill = compact_ge(c, fill, T, cc);
+        const ChunkCounts cc = count_chunks_ge(c, B, fill, T);
+        fill = compact_ge(c, B, fill, T, cc);
         Tc = T;
         ++raises;
     }
-    par = c.par;
     return rc;
 }
 
-// Streaming pass over one row: scalar head/tail exactly, then the body tiles from the
-// ring.  Collects B ⊇ {key >= Tc} (superset only by NaN / -0-against-+0 entries, which
-// every later step filters by key), raising Tc on overflow.  Returns 0, or 1 on massive
-// ties.
-__device__ __forceinline__ int stream_collect(Ctx& c, const RowGeom& g, const Ring& ring, int t_start, uint32_t& Tc,
-                                              int& fill, int K, const GvrParams& prm, RowStats& st, uint32_t& kmax_local,
-                                              uint32_t& extras)
+// Append the elements of `mask` (round elements at sp[lb + rel_off(e)], row index
+// ibase + rel_off(e)) to B at pos, pos+1, ...
+__device__ __forceinline__ void write_candidates(const Buf& B, const float* sp, int lb, int ibase, uint32_t mask,
+                                                 int pos, uint32_t Tc, uint32_t& kmax, uint32_t& extras)
 {
-    uint32_t* bkey = s_bkey();
-    int32_t* bidx = s_bidx();
-    if (t_start == 0) {  // scalar head [0, head) and tail [body_end, n): <= 6 elements, exact key test
-        fill = 0;
+    while (mask) {
+        const int e = 31 - __clz(mask);
+        mask ^= 1u << e;
+        const int o = rel_off(e);
+        const uint32_t u = __float_as_uint(sp[lb + o]);
+        const uint32_t kv = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);  // f2key
+        kmax = max(kmax, kv);
+        extras += kv < Tc;  // superset entry (NaN / -0 against +0)
+        B.key[pos] = kv;
+        B.idx[pos] = ibase + o;
+        ++pos;
+    }
+}
+
+// The streaming pass of one row (row body through the ring; the <= 6 unaligned head /
+// tail scalars exactly).  Collects B ⊇ {key >= Tc}, superset only by NaN / -0-against-+0
+// entries counted in `extras`.  Returns 0, or 1 on massive ties (the remaining tiles are
+// still waited for, so no copy is in flight when the ring is reused).
+__device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const RowPlan& p, const Buf& B,
+                                          int32_t* rhist, uint32_t& Tc, int& fill, int K, int& raises, uint32_t& kmax,
+                                          uint32_t& extras)
+{
+    int* fillp = c.misc + 16;     // reservation cursor
+    int* failbase = c.misc + 17;  // lowest failed reservation of the round
+    const int body_end = p.head + p.nfl;
+    {  // scalar head [0, head) and tail [body_end, n)
+        const int tail = p.n - body_end;
         int i = -1;
-        if (c.tid < g.head)
+        if (c.tid < p.head)
             i = c.tid;
-        else if (c.tid < g.head + g.tail)
-            i = g.body_end + (c.tid - g.head);
-        const uint32_t kv = i >= 0 ? f2key(__ldg(g.x + i)) : 0u;
+        else if (c.tid < p.head + tail)
+            i = body_end + (c.tid - p.head);
+        const uint32_t kv = i >= 0 ? f2key(__ldg(p.x + i)) : 0u;
         const uint32_t pass = (i >= 0 && kv >= Tc) ? 1u : 0u;
         uint32_t tot;
-        const uint32_t ex = block_excl_scan(c, pass, tot);
+        const uint32_t ex = group_excl_scan(c, pass, tot);
         if (pass) {
-            bkey[ex] = kv;
-            bidx[ex] = i;
+            B.key[ex] = kv;
+            B.idx[ex] = i;
+            kmax = max(kmax, kv);
         }
-        fill = (int)tot;
+        if (c.tid == 0) {
+            *fillp = (int)tot;
+            *failbase = 0x7fffffff;
+        }
+        c.sync();
     }
-    const float inv_n = 1.0f / (float)g.n;
+    const int lb = lane_base(c.warp, c.lane);
+    const float inv_n = 1.0f / (float)p.n;
+    const int nrounds = (p.ntiles + ROUND_STAGES - 1) / ROUND_STAGES;
     float Tf = key2f(Tc);
-    for (int t = t_start; t < ring.ntiles; ++t) {
-        ring.wait(t);
-        const float* sp = ring.stage_ptr(t);
-        const int nf = ring.tile_floats(t);
-        uint32_t vmask = 0xffffu;
-        if (nf != STAGE_FLOATS) {
-            vmask = 0u;
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-                if (tile_pos(c.tid, e) < nf) vmask |= 1u << e;
-        }
+    int rc = 0;
+    for (int rd = 0; rd < nrounds; ++rd) {
+        const int t0 = rd * ROUND_STAGES;
+        const int s0 = t0 % NSTAGE;
+        const uint32_t par = (uint32_t)(t0 / NSTAGE) & 1u;
+        const int nf = min(ROUND_FLOATS, p.nfl - t0 * STAGE_FLOATS);  // floats in this round
+        mbar_wait(ring.full(s0), par);
+        if (t0 + 1 < p.ntiles) mbar_wait(ring.full(s0 + 1), par);
+        const float* sp = ring.stage(s0);
+        const int ibase = p.head + t0 * STAGE_FLOATS + lb;
+        bool failed_here = false;
         uint32_t mask = 0;
+        if (rc == 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float4 v = reinterpret_cast<const float4*>(sp)[c.tid + j * NT];
-            if (pass_ge(v.x, Tf)) mask |= 1u << (4 * j);
-            if (pass_ge(v.y, Tf)) mask |= 2u << (4 * j);
-            if (pass_ge(v.z, Tf)) mask |= 4u << (4 * j);
-            if (pass_ge(v.w, Tf)) mask |= 8u << (4 * j);
-        }
-        mask &= vmask;
-        uint32_t tot;
-        uint32_t ex = block_excl_scan(c, (uint32_t)__popc(mask), tot);
-        // every thread is past tile t-1: refill its stage with tile t-1+NSTAGE
-        if (c.tid == 0 && t >= 1 && t - 1 + NSTAGE < ring.ntiles) ring.issue(t - 1 + NSTAGE);
-        if (fill + (int)tot > CAP) {  // block-uniform
-            const float phi = (float)(g.head + g.tail + t * STAGE_FLOATS + nf) * inv_n;
-            if (raise_threshold(sp, vmask, Tc, fill, (uint32_t)fill + tot, phi, K, prm.max_secant, st.raises, c.par))
-                return 1;
-            extras = 0;  // the compaction was exact
-            Tf = key2f(Tc);
-            mask = 0;
-            for (int e = 0; e < 16; ++e)
-                if (((vmask >> e) & 1u) && f2key(sp[tile_pos(c.tid, e)]) >= Tc) mask |= 1u << e;
-            ex = block_excl_scan(c, (uint32_t)__popc(mask), tot);
-        }
-        // write the (few) candidates, picked out of the stage by index
-        int pos = fill + (int)ex;
-        const int ebase = g.head + t * STAGE_FLOATS;
-        while (mask) {
-            const int e = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int q = tile_pos(c.tid, e);
-            const uint32_t kv = f2key(sp[q]);
-            kmax_local = max(kmax_local, kv);
-            extras += kv < Tc;  // superset entry (NaN / -0 against +0)
-            bkey[pos] = kv;
-            bidx[pos] = ebase + q;
-            ++pos;
-        }
-        fill += (int)tot;
-    }
-    return 0;
-}
-
-// Capture the scalar head/tail and the whole first ring tile into B unfiltered (the
-// collect threshold is not known yet: Phase 1's gathers are still in flight).  Tile 0
-// keeps its stage layout, so B[0, nf0) is contiguous; the <= 6 scalars follow.
-// Returns the fill.
-__device__ __forceinline__ int capture_first_tile(Ctx& c, const RowGeom& g, const Ring& ring, uint32_t& kmax_local)
-{
-    uint32_t* bkey = s_bkey();
-    int32_t* bidx = s_bidx();
-    int nf0 = 0;
-    if (ring.ntiles > 0) {
-        ring.wait(0);
-        nf0 = ring.tile_floats(0);
-        const float4* sp = reinterpret_cast<const float4*>(ring.stage_ptr(0));
+            for (int j = 0; j < 8; ++j) {
+                const float4 v = *reinterpret_cast<const float4*>(sp + lb + 128 * j);
+                mask |= (uint32_t)pass_ge(v.x, Tf) << (4 * j);
+                mask |= (uint32_t)pass_ge(v.y, Tf) << (4 * j + 1);
+                mask |= (uint32_t)pass_ge(v.z, Tf) << (4 * j + 2);
+                mask |= (uint32_t)pass_ge(v.w, Tf) << (4 * j + 3);
+            }
+            if (nf != ROUND_FLOATS) {
+                uint32_t vm = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int v = c.tid + j * NT;
-            if (4 * v < nf0) {
-                const float4 f = sp[v];
-                const uint4 kk = make_uint4(f2key(f.x), f2key(f.y), f2key(f.z), f2key(f.w));
-                kmax_local = max(kmax_local, max(max(kk.x, kk.y), max(kk.z, kk.w)));
-                reinterpret_cast<uint4*>(bkey)[v] = kk;
-                const int i0 = g.head + 4 * v;
-                reinterpret_cast<int4*>(bidx)[v] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+                for (int j = 0; j < 8; ++j)
+                    if (lb + 128 * j < nf) vm |= 0xfu << (4 * j);
+                mask &= vm;
+            }
+            const uint32_t cnt = (uint32_t)__popc(mask);
+            const uint32_t incl = warp_incl_scan(cnt, c.lane);
+            const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+            int base = 0;
+            if (c.lane == 31 && wtot) base = atomicAdd(fillp, (int)wtot);
+            base = __shfl_sync(FULL, base, 31);
+            if (wtot && base + (int)wtot > B.cap) {  // warp-uniform: no room, hold the round
+                failed_here = true;
+                if (c.lane == 0) atomicMin(failbase, base);
+            } else {
+                write_candidates(B, sp, lb, ibase, mask, base + (int)(incl - cnt), Tc, kmax, extras);
             }
         }
-    }
-    const int ns = g.head + g.tail;  // <= 6
-    if (c.tid < ns) {
-        const int i = c.tid < g.head ? c.tid : g.body_end + (c.tid - g.head);
-        const uint32_t kv = f2key(__ldg(g.x + i));
-        kmax_local = max(kmax_local, kv);
-        bkey[nf0 + c.tid] = kv;
-        bidx[nf0 + c.tid] = i;
-    }
-    return nf0 + ns;
-}
-
-// Phase 4 over the candidates B[0, cand): returns T*, the exact
-// K-th largest key, and n>=(T*).  Level 0: 2048-bin histogram over [kmin, kmax] with
-// power-of-two bin width, warp-parallel K-th-bin search, T = lower edge of the K-th
-// bin, then snap iterations until n>(T) < K <= n>=(T).  All snap steps stay inside
-// the K-th bin, so they are computed by one warp over that bin's members plus the
-// count above the bin.  A bin too large for the member list is re-histogrammed.
-__device__ __forceinline__ uint32_t refine_exact(Ctx& c, int cand, int K, uint32_t kmin, uint32_t kmax, uint32_t& nge_out,
-                                                 RowStats& st)
-{
-    const uint32_t* bkey = s_bkey();
-    int32_t* hist = s_hist();
-    uint32_t* list = s_list();
-    int32_t* misc = s_misc();
-    uint32_t base = kmin;
-    uint64_t width = (uint64_t)kmax - kmin + 1ull;  // keys in [base, base + width)
-    int s = shift_for_width(width);
-    uint32_t krem = (uint32_t)K, above = 0;
-    for (int level = 0; level < 5; ++level) {
-        zero_hist(c, hist, NBINS);
-        if (c.tid == 0) misc[4] = 0;
-        csync();
-        for (int p = c.tid; p < cand; p += NT) {
-            const uint32_t k = bkey[p];
-            if (k >= base && (uint64_t)(k - base) < width) atomicAdd(&hist[(k - base) >> s], 1);
-        }
-        csync();
-        int b;
-        uint32_t a;
-        kth_bin(c, NBINS, krem, b, a);
-        const uint32_t hb = (uint32_t)hist[b];
-        const uint32_t lo_b = base + ((uint32_t)b << s);
-        above += a;
-        krem -= a;
-        if (s == 0) {
-            nge_out = above + hb;
-            return lo_b;
-        }
-        const uint64_t bw = 1ull << s;
-        if (hb <= (uint32_t)LIST_MAX) {
-            for (int p = c.tid; p < cand; p += NT) {
-                const uint32_t k = bkey[p];
-                if (k >= lo_b && (uint64_t)(k - lo_b) < bw) list[atomicAdd(&misc[4], 1)] = k;
-            }
-            csync();
-            if (c.warp == 0) {
-                // snap iterations, T starts at the bin's lower edge
-                uint32_t T = lo_b, nge = 0;
-                int S = 0;
-                for (;;) {
-                    uint32_t ge = 0, gt = 0, up = 0xffffffffu, dn = 0u;
-                    for (int i = c.lane; i < (int)hb; i += 32) {
-                        const uint32_t k = list[i];
-                        ge += k >= T;
-                        gt += k > T;
-                        if (k > T) up = min(up, k);
-                        if (k < T) dn = max(dn, k);
-                    }
-                    ge = above + __reduce_add_sync(FULL, ge);
-                    gt = above + __reduce_add_sync(FULL, gt);
-                    up = __reduce_min_sync(FULL, up);
-                    dn = __reduce_max_sync(FULL, dn);
-                    ++S;
-                    if (ge < (uint32_t)K && dn >= lo_b)
-                        T = dn;
-                    else if (gt >= (uint32_t)K)
-                        T = up;
-                    else {
-                        nge = ge;
-                        break;
-                    }
+        if (c.sync_or(failed_here)) {
+            // B would overflow: raise T_c over B and the held elements, then the held
+            // warps filter their elements again and append them.
+            int f = min(*fillp, *failbase);
+            const float phi = (float)(p.n - p.nfl + t0 * STAGE_FLOATS + nf) * inv_n;
+            const uint32_t held = failed_here ? mask : 0u;
+            uint32_t mx = kmax;
+            for (uint32_t m = held; m; m &= m - 1) mx = max(mx, f2key(sp[lb + rel_off(__ffs(m) - 1)]));
+            mx = group_red1<R_MAX>(c, mx);
+            const int rr = raise_threshold(c, B, rhist, sp, lb, held, Tc, f, mx, phi, K, raises);
+            if (rr) {
+                rc = 1;
+            } else {
+                extras = 0;  // the compaction was exact
+                Tf = key2f(Tc);
+                if (c.tid == 0) {
+                    *fillp = f;
+                    *failbase = 0x7fffffff;
                 }
-                if (c.lane == 0) {
-                    misc[6] = (int32_t)T;
-                    misc[7] = (int32_t)nge;
-                    misc[8] = S;
+                c.sync();
+                if (failed_here) {
+                    uint32_t m2 = 0;
+                    for (uint32_t m = mask; m; m &= m - 1) {
+                        const int e = __ffs(m) - 1;
+                        if (f2key(sp[lb + rel_off(e)]) >= Tc) m2 |= 1u << e;
+                    }
+                    const uint32_t cnt = (uint32_t)__popc(m2);
+                    const uint32_t incl = warp_incl_scan(cnt, c.lane);
+                    const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+                    int base = 0;
+                    if (c.lane == 31 && wtot) base = atomicAdd(fillp, (int)wtot);
+                    base = __shfl_sync(FULL, base, 31);
+                    write_candidates(B, sp, lb, ibase, m2, base + (int)(incl - cnt), Tc, kmax, extras);
                 }
             }
-            csync();
-            nge_out = (uint32_t)misc[7];
-            st.snap += misc[8];
-            const uint32_t Tstar = (uint32_t)misc[6];
-            csync();  // misc reused by the caller
-            return Tstar;
+            c.sync();
         }
-        // exact narrowing inside bin b
-        base = lo_b;
-        width = bw;
-        s = s > 11 ? s - 11 : 0;
+        if (c.tid == 0)
+#pragma unroll
+            for (int q = 0; q < ROUND_STAGES; ++q)
+                if (t0 + q + NSTAGE < p.ntiles) ring.issue(p, t0 + q + NSTAGE);
     }
-    nge_out = 0;
-    return base;  // unreachable: s reaches 0 within 3 narrowing levels
+    fill = *fillp;
+    c.sync();  // every thread has read the cursor before the scratch is reused
+    return rc;
 }
 
-// Phase timestamps: clock64() at phase boundaries, written by thread 0 when `phase_ts`
-// is non-null (the paper's -DGVR_PHASE_TIMING instrumentation).
-enum { TS_START = 0, TS_PHASE1, TS_STREAM, TS_PHASE23, TS_PHASE4, TS_END, TS_N };
-
-__global__ void __launch_bounds__(NT, 2)
-gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens,
-                const int32_t* prev, int k, int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm,
-                long long* phase_ts)
+// Phases 2-4 and the ordered output of one streamed row.
+// st = {secant_iters, snap_iters, cand_count, needs_tiefill}.
+__device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work& Wk, const RowMeta& meta,
+                                           const GvrParams& prm, int k, int32_t* o, float* ov, int (&st)[4],
+                                           long long* ts)
 {
-    long long ts[TS_N] = {0, 0, 0, 0, 0, 0};
-    if (phase_ts) ts[TS_START] = clock64();
-    Ctx c = make_ctx();
+    const int K = k;
+    const int fill = meta.fill;
+    const uint32_t Tc = meta.Tc;
+    const uint32_t ftc = meta.ftc;
+    const uint32_t kmax = meta.kmax;
+    const uint32_t extras = meta.extras;
+    const uint32_t T0 = meta.T0;
+    const bool t0_ok = meta.t0_ok;
+    st[0] = 1;  // f(T_c) was counted during the stream
+    // ---------------- Phase 2: secant search over B
+    uint32_t T = Tc;
+    ChunkCounts cc;
+    if (ftc > (uint32_t)CWIN) {
+        uint64_t lo = Tc, hi = (uint64_t)kmax + 1ull;  // kmax = max key in B
+        uint32_t clo = ftc, chi = 0;
+        const float target = 0.5f * (float)(K + CWIN);  // f_target
+        bool have_t0 = t0_ok && (uint64_t)T0 > lo && (uint64_t)T0 < hi;
+        bool first_secant = true;
+        for (int it = 0;; ++it) {
+            if (hi - lo < 2 || it >= 64) {
+                T = (uint32_t)lo;  // f(lo) <= cap: B itself is a valid candidate set
+                cc = count_chunks_ge(c, B, fill, T);
+                break;
+            }
+            if (have_t0) {
+                T = T0;  // Phase 2 starts at T0 = pmean
+                have_t0 = false;
+            } else {
+                T = secant_step(lo, clo, hi, chi, target, first_secant, it >= prm.max_secant);
+                first_secant = false;
+            }
+            cc = count_chunks_ge(c, B, fill, T);
+            const uint32_t f = group_red1<R_ADD>(c, chunk_total(cc));
+            ++st[0];
+            if (f >= (uint32_t)K && f <= (uint32_t)CWIN) break;
+            if (f > (uint32_t)CWIN) {
+                lo = T;
+                clo = f;
+            } else {
+                hi = T;
+                chi = f;
+            }
+        }
+    }
+    // ---------------- Phase 3: ballot-free compaction
+    int cand = fill;
+    if (T != Tc) {
+        cand = compact_ge(c, B, fill, T, cc);
+    } else if (extras != 0u) {
+        cc = count_chunks_ge(c, B, fill, T);
+        cand = compact_ge(c, B, fill, T, cc);
+    }
+    st[2] = cand;
+    if (ts) ts[TS_PHASE23] = clock64();
+    // ---------------- Phase 4: exact refinement
+    // every candidate key lies in [T, kmax] (kmax tracked while collecting)
+    uint32_t Tstar = T, nge = (uint32_t)cand;
+    if (cand != K) {
+        int32_t* hist = Wk.hist;
+        uint32_t* list = Wk.list();
+        uint32_t base = T;
+        uint64_t width = (uint64_t)kmax - T + 1ull;  // keys in [base, base + width)
+        int s = shift_for_width(width);
+        uint32_t krem = (uint32_t)K, above = 0;
+        for (int level = 0; level < 5; ++level) {
+            zero_ints(c, hist, NBINS);
+            if (c.tid == 0) c.misc[4] = 0;
+            c.sync();
+            for (int p = c.tid; p < cand; p += GVR_NT) {
+                const uint32_t kk = B.key[p];
+                if (kk >= base && (uint64_t)(kk - base) < width) atomicAdd(&hist[(kk - base) >> s], 1);
+            }
+            c.sync();
+            int b;
+            uint32_t a;
+            kth_bin(c, hist, NBINS, krem, b, a);
+            const uint32_t hb = (uint32_t)hist[b];
+            const uint32_t lo_b = base + ((uint32_t)b << s);
+            above += a;
+            krem -= a;
+            if (s == 0) {
+                Tstar = lo_b;
+                nge = above + hb;
+                break;
+            }
+            const uint64_t bw = 1ull << s;
+            if (hb <= (uint32_t)LIST_MAX) {
+                for (int p = c.tid; p < cand; p += GVR_NT) {
+                    const uint32_t kk = B.key[p];
+                    if (kk >= lo_b && (uint64_t)(kk - lo_b) < bw) list[atomicAdd(&c.misc[4], 1)] = kk;
+                }
+                c.sync();
+                if (c.warp == 0) {
+                    // snap iterations, T starts at the bin's lower edge
+                    uint32_t Ts = lo_b, ge_f = 0;
+                    int S = 0;
+                    for (;;) {
+                        uint32_t ge = 0, gt = 0, up = 0xffffffffu, dn = 0u;
+                        for (int i = c.lane; i < (int)hb; i += 32) {
+                            const uint32_t kk = list[i];
+                            ge += kk >= Ts;
+                            gt += kk > Ts;
+                            if (kk > Ts) up = min(up, kk);
+                            if (kk < Ts) dn = max(dn, kk);
+                        }
+                        ge = above + __reduce_add_sync(FULL, ge);
+                        gt = above + __reduce_add_sync(FULL, gt);
+                        up = __reduce_min_sync(FULL, up);
+                        dn = __reduce_max_sync(FULL, dn);
+                        ++S;
+                        if (ge < (uint32_t)K && dn >= lo_b)
+                            Ts = dn;
+                        else if (gt >= (uint32_t)K)
+                            Ts = up;
+                        else {
+                            ge_f = ge;
+                            break;
+                        }
+                    }
+                    if (c.lane == 0) {
+                        c.misc[6] = (int32_t)Ts;
+                        c.misc[7] = (int32_t)ge_f;
+                        c.misc[8] = S;
+                    }
+                }
+                c.sync();
+                Tstar = (uint32_t)c.misc[6];
+                nge = (uint32_t)c.misc[7];
+                st[1] += c.misc[8];
+                c.sync();
+                break;
+            }
+            // exact narrowing inside bin b
+            base = lo_b;
+            width = bw;
+            s = s > 11 ? s - 11 : 0;
+        }
+    } else {
+        uint32_t kmin = 0xffffffffu;
+        for (int q = c.tid; q < cand; q += GVR_NT) kmin = min(kmin, B.key[q]);
+        Tstar = group_red1<R_MIN>(c, kmin);
+    }
+    if (ts) ts[TS_PHASE4] = clock64();
+    // ---------------- ordered output
+    if (nge > (uint32_t)SORT_MAX) {
+        st[3] = 1;  // the caller runs the ordered tie fill from global memory
+        uint32_t ngt = 0;
+        for (int q = c.tid; q < cand; q += GVR_NT) ngt += B.key[q] > Tstar;
+        ngt = group_red1<R_ADD>(c, ngt);
+        if (c.tid == 0) {
+            c.misc[10] = (int32_t)Tstar;
+            c.misc[11] = (int32_t)ngt;
+        }
+        c.sync();
+    } else {
+        st[3] = 0;
+        emit_sorted(c, B, Wk, cand, Tstar, kmax, (int)nge, K, k, o, ov);
+    }
+}
+
+
+__global__ void __launch_bounds__(GVR_NT, 2)
+gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, const int32_t* prev,
+                int k, int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, long long* phase_ts)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
     const int r = blockIdx.x;
-    int n = (int)stride;
-    if (row_lens) n = min(max(__ldg(row_lens + r), 0), (int)stride);
-    const float* x = scores + (int64_t)r * stride;
+    const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
+                    policy_evict_first()};
+    const Buf B{reinterpret_cast<uint32_t*>(smem + G_OFF_B), reinterpret_cast<int32_t*>(smem + G_OFF_B + GVR_CAP * 4),
+                GVR_CAP};
+    const Work Wk{reinterpret_cast<int32_t*>(smem + G_OFF_WORK), reinterpret_cast<int32_t*>(smem + G_OFF_WORK + NBINS * 4),
+                  reinterpret_cast<unsigned long long*>(smem + G_OFF_WORK + 2 * NBINS * 4), GVR_CSORT};
+    GvrGroup c;
+    c.init(threadIdx.x, smem + G_OFF_SCR);
+    const int K = k;
+    const RowPlan p = plan_row(scores, stride, row_lens, r, k);
+    const long long ts0 = phase_ts ? clock64() : 0ll;
+    if (c.tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(ring.full(s), 1);
+        fence_mbar_init();
+        for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);  // the first 64 KB load during Phase 1
+    }
+    const RowGeom g = make_geom(p.x, p.n);
     int32_t* o = out + (int64_t)r * k;
     float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
-    const RowGeom g = make_geom(x, n);
-    RowStats st = {0, 0, 0, GVR_DONE_CONVERGED, 0, 0, 0};
-    const int K = k;
-
-    if (n <= k) {
-        // no selection needed; the guess is irrelevant (every element is emitted)
-        small_row_emit(c, g, k, o, ov);
-        st.done = GVR_DONE_TRIVIAL;
-        st.passes = 1;
-        st.cand = n;
+    int st[4] = {0, 0, 0, 0};
+    int done_kind = GVR_DONE_CONVERGED, passes = 1, raises = 0, ftc_stat = 0;
+    long long tsr[TS_N] = {ts0, 0, 0, 0, 0, 0};
+    if (p.n <= k) {
+        c.sync();
+        small_row_emit(c, B, Wk, g, k, o, ov);
+        done_kind = GVR_DONE_TRIVIAL;
+        st[2] = p.n;
     } else {
-        // start streaming the row body before Phase 1 (TMA ring, pipeline.cuh)
-        const Ring ring = make_ring(x + g.head, 4 * g.nvec);
-        ring_start(ring);
-
         // ---------------- Phase 1: guess statistics (Eq. 4)
-        // The gathers are issued now and consumed after the first ring tile has been
-        // captured, so their latency overlaps the first TMA transfer.
-        constexpr int GPT = KMAX / NT;  // guesses per thread
+        constexpr int GPT = KMAX / GVR_NT;  // 8 guesses per thread
+        const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
         float gv[GPT];
-        uint32_t gok = 0;
-        {
+        uint32_t valid = 0;
+        if (pr) {
             int32_t gi[GPT];
-            const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
 #pragma unroll
             for (int j = 0; j < GPT; ++j) {
-                const int q = c.tid + j * NT;
-                gi[j] = -1;
-                if (pr && q < k) asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(gi[j]) : "l"(pr + q));
+                const int q = c.tid + j * GVR_NT;
+                gi[j] = q < k ? __ldg(pr + q) : -1;
             }
 #pragma unroll
             for (int j = 0; j < GPT; ++j) {
                 gv[j] = 0.f;
-                if (gi[j] >= 0 && gi[j] < n) {
-                    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(gv[j]) : "l"(x + gi[j]));
-                    gok |= 1u << j;
+                if (gi[j] >= 0 && gi[j] < p.n) {
+                    gv[j] = __ldg(p.x + gi[j]);
+                    valid |= 1u << j;
                 }
             }
         }
-        csync();  // ring barriers initialised before anyone waits on them
-        uint32_t kmax_local = 0u, extras = 0u;
-        int fill = capture_first_tile(c, g, ring, kmax_local);
         uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
         float sum = 0.f, sq = 0.f;
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
-            if ((gok >> j) & 1u) {
-                const float v = gv[j];
-                const uint32_t kv = f2key(v);
+            if ((valid >> j) & 1u) {
+                const uint32_t kv = f2key(gv[j]);
                 kmn = min(kmn, kv);
                 kmx = max(kmx, kv);
                 ++cnt;
-                sum += v;
-                sq += v * v;
+                sum += gv[j];
+                sq += gv[j] * gv[j];
             }
         }
-        block_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+        group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);  // (also publishes the barrier init)
         if (cnt == 0) {
             // no valid guess: deterministic stride sample of M values
             kmn = 0xffffffffu;
             kmx = 0u;
             sum = sq = 0.f;
-            const int M = min(KMAX, n);
-            for (int j = c.tid; j < M; j += NT) {
-                const int q = (int)(((int64_t)j * n) / M);
-                const float v = __ldg(x + q);
+            const int M = min(KMAX, p.n);
+            for (int j = c.tid; j < M; j += GVR_NT) {
+                const int q = (int)(((int64_t)j * p.n) / M);
+                const float v = __ldg(p.x + q);
                 const uint32_t kv = f2key(v);
                 kmn = min(kmn, kv);
                 kmx = max(kmx, kv);
@@ -435,124 +585,62 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
                 sum += v;
                 sq += v * v;
             }
-            block_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+            group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
         }
-        block_fsum2(c, sum, sq);
+        group_fsum2(c, sum, sq);
         const float pmean = sum / (float)cnt;
         const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
         const float tcf = pmean - prm.collect_sigma * sqrtf(var);
-        uint32_t Tc = isfinite(tcf) ? f2key(tcf) : kmn;
-        if (n <= CAP) Tc = 0u;  // the whole row fits in B
-        const uint32_t T0 = f2key(pmean);
-        const bool t0_ok = isfinite(pmean);
-
+        RowMeta m;
+        m.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
+        if (p.n <= B.cap) m.Tc = 0u;  // the whole row fits in B
+        m.T0 = f2key(pmean);
+        m.t0_ok = isfinite(pmean);
+        if (phase_ts) tsr[TS_PHASE1] = clock64();
         // ---------------- streaming pass (HBM read once, TMA ring)
-        if (phase_ts) ts[TS_PHASE1] = clock64();
-        ++st.passes;
-        if (Tc != 0u) {  // apply T_c to the captured first tile
-            const ChunkCounts c0 = count_chunks_ge(c, fill, Tc);
-            fill = compact_ge(c, fill, Tc, c0);
-        }
-        const int rc = stream_collect(c, g, ring, 1, Tc, fill, K, prm, st, kmax_local, extras);
-        uint32_t kmax = kmax_local;
-        block_red2<R_MAX, R_ADD>(c, kmax, extras);  // also: B complete and visible
-        const uint32_t ftc = rc == 0 ? (uint32_t)fill - extras : 0u;  // exact f(T_c)
-        if (phase_ts) ts[TS_STREAM] = clock64();
-        ChunkCounts cc;
-        if (rc != 0 || ftc < (uint32_t)K) {
+        uint32_t kmax = 0u, extras = 0u;
+        const int rc = stream_row(c, ring, p, B, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST), m.Tc, m.fill, K, raises,
+                                  kmax, extras);
+        group_red2<R_MAX, R_ADD>(c, kmax, extras);
+        m.kmax = kmax;
+        m.extras = extras;
+        m.ftc = (uint32_t)m.fill - extras;
+        if (phase_ts) tsr[TS_STREAM] = clock64();
+        if (rc || m.ftc < (uint32_t)K) {
             // massive ties, or f(T_c) < K (the guess overshot): exact radix select +
             // ordered tie fill from global memory (R12/R13)
-            const RadixResult rr = radix_select_global(c, g, (uint32_t)K, false);
-            st.passes += rr.rounds + 1;
-            st.done = GVR_DONE_TIEFILL;
-            tiefill_emit(c, g, rr.prefix, rr.above, K, k, o, ov);
+            const RadixResult rr = radix_select_global(c, Wk, g, (uint32_t)K, false);
+            passes += rr.rounds + 1;
+            done_kind = GVR_DONE_TIEFILL;
+            tiefill_emit(c, B, Wk, g, rr.prefix, rr.above, K, k, o, ov);
         } else {
-            st.bufcnt = (int)ftc;
-            st.secant = 1;  // f(T_c) was counted during the stream
-            // ---------------- Phase 2: secant search over B
-            uint32_t T = Tc;
-            if (ftc > (uint32_t)CWIN) {
-                uint64_t lo = Tc, hi = (uint64_t)kmax + 1ull;  // kmax = max key in B
-                uint32_t clo = ftc, chi = 0;
-                const float target = 0.5f * (float)(K + CWIN);  // f_target
-                bool have_t0 = t0_ok && (uint64_t)T0 > lo && (uint64_t)T0 < hi;
-                bool first_secant = true;
-                for (int it = 0;; ++it) {
-                    if (hi - lo < 2 || it >= 64) {
-                        T = (uint32_t)lo;  // f(lo) <= CAP: B itself is a valid candidate set
-                        cc = count_chunks_ge(c, fill, T);
-                        break;
-                    }
-                    if (have_t0) {
-                        T = T0;  // Phase 2 starts at T0 = pmean
-                        have_t0 = false;
-                    } else {
-                        T = secant_step(lo, clo, hi, chi, target, first_secant, it >= prm.max_secant);
-                        first_secant = false;
-                    }
-                    cc = count_chunks_ge(c, fill, T);
-                    const uint32_t f = block_red1<R_ADD>(c, chunk_total(cc));
-                    ++st.secant;
-                    if (f >= (uint32_t)K && f <= (uint32_t)CWIN) break;
-                    if (f > (uint32_t)CWIN) {
-                        lo = T;
-                        clo = f;
-                    } else {
-                        hi = T;
-                        chi = f;
-                    }
-                }
-            }
-            // ---------------- Phase 3: ballot-free compaction
-            int cand = fill;
-            if (T != Tc) {
-                cand = compact_ge(c, fill, T, cc);
-            } else if (extras != 0u) {
-                cc = count_chunks_ge(c, fill, T);
-                cand = compact_ge(c, fill, T, cc);
-            }
-            st.cand = cand;
-            if (phase_ts) ts[TS_PHASE23] = clock64();
-            // ---------------- Phase 4: exact refinement
-            // every candidate key lies in [T, kmax] (kmax tracked while collecting)
-            uint32_t Tstar = T, nge = (uint32_t)cand;
-            if (cand != K) {
-                Tstar = refine_exact(c, cand, K, T, kmax, nge, st);
-            } else {
-                uint32_t kmin = 0xffffffffu;
-                for (int q = c.tid; q < cand; q += NT) kmin = min(kmin, s_bkey()[q]);
-                Tstar = block_red1<R_MIN>(c, kmin);
-            }
-            if (phase_ts) ts[TS_PHASE4] = clock64();
-            // ---------------- ordered output
-            if (nge > (uint32_t)SORT_MAX) {
+            ftc_stat = (int)m.ftc;
+            refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
+            if (st[3]) {
                 // huge tie group at T*: ordered tie fill from global memory (R13)
-                uint32_t ngt = 0;
-                for (int q = c.tid; q < cand; q += NT) ngt += s_bkey()[q] > Tstar;
-                ngt = block_red1<R_ADD>(c, ngt);
-                st.done = GVR_DONE_TIEFILL;
-                ++st.passes;
-                tiefill_emit(c, g, Tstar, ngt, K, k, o, ov);
-            } else {
-                emit_sorted(c, cand, Tstar, kmax, (int)nge, K, k, o, ov);
+                done_kind = GVR_DONE_TIEFILL;
+                ++passes;
+                tiefill_emit(c, B, Wk, g, (uint32_t)c.misc[10], (uint32_t)c.misc[11], K, k, o, ov);
             }
         }
     }
-    if (phase_ts && c.tid == 0) {
-        ts[TS_END] = clock64();
-        for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = ts[i];
-    }
-    if (stats && c.tid == 0) {
-        gvr_row_stats s;
-        s.secant_iters = st.secant;
-        s.snap_iters = st.snap;
-        s.cand_count = st.cand;
-        s.done_kind = st.done;
-        s.global_passes = st.passes;
-        s.raises = st.raises;
-        s.buffer_count = st.bufcnt;
-        s.cluster = 1;
-        stats[r] = s;
+    if (c.tid == 0) {
+        if (stats) {
+            gvr_row_stats s;
+            s.secant_iters = st[0];
+            s.snap_iters = st[1];
+            s.cand_count = st[2];
+            s.done_kind = done_kind;
+            s.global_passes = passes;
+            s.raises = raises;
+            s.buffer_count = ftc_stat;
+            s.cluster = 1;
+            stats[r] = s;
+        }
+        if (phase_ts) {
+            tsr[TS_END] = clock64();
+            for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = tsr[i];
+        }
     }
 }
 

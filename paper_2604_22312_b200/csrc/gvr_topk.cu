@@ -10,6 +10,8 @@ namespace {
 
 using namespace gvr;
 
+thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+
 constexpr int kVersion = 1 * 10000 + 0 * 100 + 0;
 
 bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb)
@@ -33,15 +35,18 @@ gvr_status set_smem(Kern kern, int bytes)
 {
     // Opt in to > 48 KB dynamic shared memory; idempotent and cheap.
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
-        (void)cudaGetLastError();
+        g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
     return GVR_OK;
 }
 
+
 gvr_status launch_status()
 {
-    return cudaGetLastError() == cudaSuccess ? GVR_OK : GVR_ERR_CUDA;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) g_last_cuda_error = e;
+    return e == cudaSuccess ? GVR_OK : GVR_ERR_CUDA;
 }
 
 }  // namespace
@@ -61,6 +66,29 @@ const char* gvr_status_string(gvr_status s)
 
 int32_t gvr_version(void) { return kVersion; }
 
+gvr_status gvr_kernel_info(int32_t* gvr_ctas_per_sm, int32_t* gvr_threads, int32_t* gvr_smem_bytes,
+                           int32_t* radix_ctas_per_sm, int32_t* radix_threads, int32_t* radix_smem_bytes)
+{
+    gvr_status st;
+    if ((st = set_smem(gvr_topk_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;
+    if ((st = set_smem(radix_topk_kernel, RADIX_SMEM_BYTES)) != GVR_OK) return st;
+    int a = 0, b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, gvr_topk_kernel, GVR_NT, GVR_SMEM_BYTES) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, radix_topk_kernel, RADIX_NT, RADIX_SMEM_BYTES) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    if (gvr_ctas_per_sm) *gvr_ctas_per_sm = a;
+    if (gvr_threads) *gvr_threads = GVR_NT;
+    if (gvr_smem_bytes) *gvr_smem_bytes = GVR_SMEM_BYTES;
+    if (radix_ctas_per_sm) *radix_ctas_per_sm = b;
+    if (radix_threads) *radix_threads = RADIX_NT;
+    if (radix_smem_bytes) *radix_smem_bytes = RADIX_SMEM_BYTES;
+    return GVR_OK;
+}
+
+const char* gvr_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
+
 static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
                              const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
                              const gvr_options* opt, float* out_val, gvr_row_stats* stats, long long* phase_ts)
@@ -78,9 +106,10 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         if (opt->collect_sigma == opt->collect_sigma) prm.collect_sigma = opt->collect_sigma;
         if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
     }
-    if ((st = set_smem(gvr_topk_kernel, SMEM_BYTES)) != GVR_OK) return st;
-    gvr_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, prev_topk, k, out_idx,
-                                                          out_val, stats, prm, phase_ts);
+    if ((st = set_smem(gvr_topk_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;
+    // one CTA per row, two CTAs per SM
+    gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, prev_topk, k, out_idx,
+                                                                  out_val, stats, prm, phase_ts);
     return launch_status();
 }
 
@@ -115,8 +144,8 @@ gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const 
     gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
     if (st != GVR_OK) return st;
     if (num_rows == 0) return GVR_OK;
-    if ((st = set_smem(radix_topk_kernel, SMEM_BYTES)) != GVR_OK) return st;
-    radix_topk_kernel<<<num_rows, NT, SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
+    if ((st = set_smem(radix_topk_kernel, RADIX_SMEM_BYTES)) != GVR_OK) return st;
+    radix_topk_kernel<<<num_rows, RADIX_NT, RADIX_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
                                                             stats);
     return launch_status();
 }

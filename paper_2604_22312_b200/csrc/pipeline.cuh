@@ -1,18 +1,26 @@
 // pipeline.cuh — TMA bulk-copy (cp.async.bulk) ring that streams a score row from HBM
-// into shared memory (sm_100a async proxy, mbarrier transaction-count completion).
+// into shared memory (sm_100a async proxy, mbarrier transaction counts).
 //
-// The row body (16-byte aligned float4 run) is cut into ring tiles of STAGE_FLOATS
-// fp32.  One elected thread arms a stage's mbarrier with the byte count and issues
-// one 1-D bulk copy global -> shared per tile; all threads wait on the stage's parity.
-// No registers hold in-flight data (the prefetch depth is set by shared memory), and
-// tiles can be indexed dynamically: the rare candidates are picked out by index.
+// The ring has NSTAGE stages of STAGE_FLOATS fp32; stages are contiguous in shared
+// memory and are consumed ROUND_STAGES at a time ("rounds"), so one round is one
+// contiguous block of ROUND_FLOATS floats.  Thread 0 arms a stage's "full" mbarrier with
+// the byte count and issues one 1-D bulk copy global -> shared; the consumers wait on
+// "full", process the round, meet at one CTA barrier, and thread 0 refills the round's
+// stages with the tiles NSTAGE ahead.  No registers hold in-flight data; the ring is
+// primed before Phase 1 so the first NSTAGE tiles load while the guess is evaluated.
 #pragma once
-#include "row_tiles.cuh"
+#include "device_common.cuh"
 
 namespace gvr {
 
+constexpr int NSTAGE = 4;
+constexpr int ROUND_STAGES = 2;
+constexpr int STAGE_FLOATS = 4096;
+constexpr int STAGE_BYTES = STAGE_FLOATS * 4;  // 16 KB
+constexpr int ROUND_FLOATS = ROUND_STAGES * STAGE_FLOATS;
+static_assert(NSTAGE % ROUND_STAGES == 0, "a round never wraps the ring");
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint32_t bar_full(int stage) { return smem_u32(g_smem + OFF_BAR + 8 * stage); }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
 {
@@ -22,10 +30,6 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t policy)
 {
@@ -57,49 +61,46 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
     }
 }
 
-// Ring over the body of one row (non-persistent CTA): stage of tile t is t % NSTAGE
-// and its mbarrier parity (t / NSTAGE) & 1.  Thread 0 primes NSTAGE tiles and refills
-// the stage of tile t-1 with tile t-1+NSTAGE once every thread has passed tile t's
-// block scan (all reads of tile t-1 are then complete).
-struct Ring {
-    const float* body;  // 16-byte aligned start of the row body
-    int nfl;            // body floats (multiple of 4)
-    int ntiles;
-    uint64_t policy;
-
-    __device__ __forceinline__ int tile_floats(int t) const { return min(STAGE_FLOATS, nfl - t * STAGE_FLOATS); }
-    __device__ __forceinline__ int stage_of(int t) const { return t % NSTAGE; }
-    __device__ __forceinline__ const float* stage_ptr(int t) const { return s_ring() + stage_of(t) * STAGE_FLOATS; }
-    __device__ __forceinline__ void issue(int t) const
-    {
-        const int st = stage_of(t);
-        const uint32_t bytes = (uint32_t)tile_floats(t) * 4u;
-        const uint32_t bar = bar_full(st);
-        mbar_arrive_expect_tx(bar, bytes);
-        bulk_g2s(smem_u32(s_ring() + st * STAGE_FLOATS), body + (size_t)t * STAGE_FLOATS, bytes, bar, policy);
-    }
-    __device__ __forceinline__ void wait(int t) const { mbar_wait(bar_full(stage_of(t)), (uint32_t)(t / NSTAGE) & 1u); }
+// Row plan: the body [head, head + nfl) is 16-byte aligned and a multiple of 4 floats;
+// the <= 3 scalars before it and after it are handled separately.
+struct RowPlan {
+    const float* x;
+    int n;
+    int head;    // scalar elements [0, head) before the first 16-byte boundary
+    int nfl;     // body floats (multiple of 4), starting at x + head (16-byte aligned)
+    int ntiles;  // 0 for rows that are not streamed (len <= k)
 };
 
-__device__ __forceinline__ Ring make_ring(const float* body, int nfl)
+__device__ __forceinline__ RowPlan plan_row(const float* scores, int64_t stride, const int32_t* row_lens, int r, int k)
 {
-    Ring r;
-    r.body = body;
-    r.nfl = nfl;
-    r.ntiles = (nfl + STAGE_FLOATS - 1) / STAGE_FLOATS;
-    r.policy = policy_evict_first();
-    return r;
+    RowPlan p;
+    int n = (int)stride;
+    if (row_lens) n = min(max(__ldg(row_lens + r), 0), (int)stride);
+    p.x = scores + (int64_t)r * stride;
+    p.n = n;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p.x);
+    int head = (int)(((16u - (uint32_t)(a & 15u)) & 15u) >> 2);
+    if (head > n) head = n;
+    p.head = head;
+    p.nfl = 4 * ((n - head) >> 2);
+    p.ntiles = n <= k ? 0 : (p.nfl + STAGE_FLOATS - 1) / STAGE_FLOATS;
+    return p;
 }
 
-// Barrier init + prime (thread 0); the caller orders it with a CTA barrier before any
-// consumer waits.
-__device__ __forceinline__ void ring_start(const Ring& r)
-{
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTAGE; ++s) mbar_init(bar_full(s), 1);
-        fence_mbar_init();
-        for (int t = 0; t < NSTAGE && t < r.ntiles; ++t) r.issue(t);
+struct Ring {
+    float* stages;   // NSTAGE * STAGE_FLOATS, contiguous
+    uint64_t* bars;  // full[NSTAGE]
+    uint64_t policy;
+    __device__ __forceinline__ uint32_t full(int s) const { return smem_u32(bars + s); }
+    __device__ __forceinline__ const float* stage(int s) const { return stages + s * STAGE_FLOATS; }
+    // thread 0 only: load body tile t of row p into its stage (t % NSTAGE)
+    __device__ __forceinline__ void issue(const RowPlan& p, int t) const
+    {
+        const int s = t % NSTAGE;
+        const uint32_t bytes = (uint32_t)min(STAGE_FLOATS, p.nfl - t * STAGE_FLOATS) * 4u;
+        mbar_arrive_expect_tx(full(s), bytes);
+        bulk_g2s(smem_u32(stage(s)), p.x + p.head + (size_t)t * STAGE_FLOATS, bytes, full(s), policy);
     }
-}
+};
 
 }  // namespace gvr

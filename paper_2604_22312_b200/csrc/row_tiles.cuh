@@ -1,11 +1,13 @@
-// row_tiles.cuh — coalesced streaming of one fp32 score row in index order.
+// row_tiles.cuh — coalesced register streaming of one fp32 score row in index order
+// (used by the radix baseline and the distribution-agnostic fallbacks; the GVR hot
+// loop streams through the TMA ring of pipeline.cuh instead).
 //
 // A row x[0, n) is split into an unaligned scalar head (elements before the first
 // 16-byte boundary, < 4), a body of float4 vectors and a scalar tail (< 4).  The body
-// is consumed in tiles of TILE_VEC float4 (NT threads x VEC float4): within a tile,
-// float4 j of thread t is vector t + j*NT, so every warp load is 512 contiguous
-// bytes (128-bit vectorised, coalesced; BASELINE.json north_star).  The next tile is
-// loaded into registers while the current one is processed (register double buffer).
+// is consumed in tiles of N*VEC float4 (N threads x VEC float4): float4 j of thread t
+// is vector t + j*N, so every warp load is 512 contiguous bytes (128-bit vectorised,
+// coalesced).  The next tile is loaded into registers while the current one is
+// processed (register double buffer).
 #pragma once
 #include "device_common.cuh"
 
@@ -18,7 +20,6 @@ struct RowGeom {
     int nvec;      // float4 vectors starting at element `head`
     int body_end;  // head + 4*nvec
     int tail;      // scalar elements [body_end, n)
-    int ntiles;
 };
 
 __device__ __forceinline__ RowGeom make_geom(const float* x, int n)
@@ -33,19 +34,19 @@ __device__ __forceinline__ RowGeom make_geom(const float* x, int n)
     g.nvec = (n - head) >> 2;
     g.body_end = head + 4 * g.nvec;
     g.tail = n - g.body_end;
-    g.ntiles = (g.nvec + TILE_VEC - 1) / TILE_VEC;
     return g;
 }
 
-// One body tile held in registers: 16 keys per thread.
+// One body tile held in registers: 4*VEC keys per thread.
+template <int N>
 struct MainTile {
     static constexpr int E = 4 * VEC;
     uint32_t key[E];
     int vbase;  // first vector index of this thread's slot j=0
     int nvec;
     int head;
-    __device__ __forceinline__ bool valid(int e) const { return vbase + (e >> 2) * NT < nvec; }
-    __device__ __forceinline__ int idx(int e) const { return head + 4 * (vbase + (e >> 2) * NT) + (e & 3); }
+    __device__ __forceinline__ bool valid(int e) const { return vbase + (e >> 2) * N < nvec; }
+    __device__ __forceinline__ int idx(int e) const { return head + 4 * (vbase + (e >> 2) * N) + (e & 3); }
 };
 
 // One scalar element per thread (head or tail).
@@ -57,19 +58,21 @@ struct ScalarTile {
     __device__ __forceinline__ int idx(int) const { return i; }
 };
 
+template <int N>
 __device__ __forceinline__ void load_tile(const RowGeom& g, int t, int tid, float4 (&v)[VEC])
 {
     const float4* xv = reinterpret_cast<const float4*>(g.x + g.head);
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-        const int vi = t * TILE_VEC + j * NT + tid;
+        const int vi = t * N * VEC + j * N + tid;
         v[j] = vi < g.nvec ? ldg_stream(xv + vi) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
-__device__ __forceinline__ void to_tile(const RowGeom& g, int t, int tid, const float4 (&v)[VEC], MainTile& mt)
+template <int N>
+__device__ __forceinline__ void to_tile(const RowGeom& g, int t, int tid, const float4 (&v)[VEC], MainTile<N>& mt)
 {
-    mt.vbase = t * TILE_VEC + tid;
+    mt.vbase = t * N * VEC + tid;
     mt.nvec = g.nvec;
     mt.head = g.head;
 #pragma unroll
@@ -81,52 +84,39 @@ __device__ __forceinline__ void to_tile(const RowGeom& g, int t, int tid, const 
     }
 }
 
-__device__ __forceinline__ ScalarTile head_tile(const RowGeom& g, int tid)
-{
-    ScalarTile s;
-    s.i = tid < g.head ? tid : -1;
-    s.key[0] = s.i >= 0 ? f2key(__ldg(g.x + s.i)) : 0u;
-    return s;
-}
-
-__device__ __forceinline__ ScalarTile tail_tile(const RowGeom& g, int tid)
-{
-    ScalarTile s;
-    s.i = tid < g.tail ? g.body_end + tid : -1;
-    s.key[0] = s.i >= 0 ? f2key(__ldg(g.x + s.i)) : 0u;
-    return s;
-}
-
 // Visit every element of the row in index order, one tile at a time:
 //   f(tile, elements_streamed_after_this_tile) -> int (non-zero aborts).
-// All threads call f for every tile (block-uniform control flow).
-template <class F>
+// All threads of the group call f for every tile (group-uniform control flow).
+template <int N, class F>
 __device__ __forceinline__ int for_each_tile(const RowGeom& g, int tid, F&& f)
 {
-    int done = 0;
     if (g.head > 0) {
-        ScalarTile s = head_tile(g, tid);
-        done += g.head;
-        int rc = f(s, done);
+        ScalarTile s;
+        s.i = tid < g.head ? tid : -1;
+        s.key[0] = s.i >= 0 ? f2key(__ldg(g.x + s.i)) : 0u;
+        const int rc = f(s, g.head);
         if (rc) return rc;
     }
-    if (g.ntiles > 0) {
+    const int ntiles = (g.nvec + N * VEC - 1) / (N * VEC);
+    if (ntiles > 0) {
         float4 cur[VEC], nxt[VEC];
-        load_tile(g, 0, tid, cur);
-        for (int t = 0; t < g.ntiles; ++t) {
-            if (t + 1 < g.ntiles) load_tile(g, t + 1, tid, nxt);
-            MainTile mt;
-            to_tile(g, t, tid, cur, mt);
-            const int vend = min(g.nvec, (t + 1) * TILE_VEC);
-            int rc = f(mt, g.head + 4 * vend);
+        load_tile<N>(g, 0, tid, cur);
+        for (int t = 0; t < ntiles; ++t) {
+            if (t + 1 < ntiles) load_tile<N>(g, t + 1, tid, nxt);
+            MainTile<N> mt;
+            to_tile<N>(g, t, tid, cur, mt);
+            const int vend = min(g.nvec, (t + 1) * N * VEC);
+            const int rc = f(mt, g.head + 4 * vend);
             if (rc) return rc;
 #pragma unroll
             for (int j = 0; j < VEC; ++j) cur[j] = nxt[j];
         }
     }
     if (g.tail > 0) {
-        ScalarTile s = tail_tile(g, tid);
-        int rc = f(s, g.n);
+        ScalarTile s;
+        s.i = tid < g.tail ? g.body_end + tid : -1;
+        s.key[0] = s.i >= 0 ? f2key(__ldg(g.x + s.i)) : 0u;
+        const int rc = f(s, g.n);
         if (rc) return rc;
     }
     return 0;

@@ -19,7 +19,9 @@ for name, (req, lay, n) in {"cfg2_batch488": (8, 61, 100_000), "batch1_N100K": (
     ok = (t[:, 1:] > 0).all(axis=1)
     d = np.diff(t[ok], axis=1)
     tot = t[ok, 5] - t[ok, 0]
-    row = {"rows": int(ok.sum()), "total_cycles_median": float(np.median(tot))}
+    row = {"rows": int(ok.sum()), "total_cycles_median": float(np.median(tot)),
+           "total_cycles_p10_p90_p99_max": [float(np.percentile(tot, q)) for q in (10, 90, 99, 100)],
+           "stream_p90_p99_max": [float(np.percentile(d[:, 1], q)) for q in (90, 99, 100)]}
     for i, ph in enumerate(gvr.PHASES):
         row[ph] = {"median": float(np.median(d[:, i])), "mean": float(d[:, i].mean()),
                    "share": float(d[:, i].sum() / tot.sum())}

@@ -1,0 +1,214 @@
+// Microbenchmark (not part of the library): GVR collect-loop variants, second round.
+//   R stages are consumed per "round": one warp scan, one shared atomic per warp for the
+//   buffer base and one CTA barrier per round, so the fixed per-round cost is spread over
+//   R * SF / NT elements per thread.  Stages are contiguous in shared memory and a round
+//   always covers R consecutive stages (NS % R == 0), so a lane's elements of a round sit
+//   at tb + 128*j + c (j = vector, c = component) of one contiguous block.
+//   The write loop walks the pass mask from the top bit (FLO) and builds the sortable key
+//   with one shift and one LOP3.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o stream_bench3 stream_bench3.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool try_wait(uint32_t bar, uint32_t par)
+{
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(bar), "r"(par)
+                 : "memory");
+    return ok;
+}
+__device__ __forceinline__ void issue(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t warp_incl(uint32_t v, int lane)
+{
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// MODE 0: mask via FSETP/SEL (compiler), MODE 1: FMNMX3 prefilter per float4 pair
+template <int NT, int NS, int SF, int R, int CAP, int MODE>
+__global__ void __launch_bounds__(NT) collect(const float* rows, int n, float tf, int* out_cnt)
+{
+    constexpr int W = NT / 32;
+    constexpr int RF = R * SF;         // floats per round
+    constexpr int EPT = RF / NT;       // elements per thread per round
+    constexpr int V = EPT / 4;         // float4 per thread per round
+    static_assert(EPT % 4 == 0 && EPT <= 32 && NS % R == 0, "");
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);
+    uint32_t* bkey = reinterpret_cast<uint32_t*>(smem + NS * SF * 4);
+    int32_t* bidx = reinterpret_cast<int32_t*>(bkey + CAP);
+    uint64_t* full = reinterpret_cast<uint64_t*>(bidx + CAP);
+    int* misc = reinterpret_cast<int*>(full + NS);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* x = rows + (size_t)blockIdx.x * n;
+    const int ntiles = n / SF;
+    const int nrounds = ntiles / R;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(smem_u32(full + s), 1);
+        misc[0] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int t = 0; t < NS && t < ntiles; ++t)
+            issue(smem_u32(ring + t * SF), x + (size_t)t * SF, SF * 4, smem_u32(full + t));
+    }
+    __syncthreads();
+    const int tb = 128 * V * warp + 4 * lane;  // lane's first float in the round block
+    for (int rd = 0; rd < nrounds; ++rd) {
+        const int s0 = (rd * R) % NS;
+        const uint32_t par = ((rd * R) / NS) & 1u;
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            while (!try_wait(smem_u32(full + s0 + q), par)) {
+            }
+        const float* sp = ring + s0 * SF;
+        uint32_t mask = 0;
+        if (MODE == 0) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const float4 v = *reinterpret_cast<const float4*>(sp + tb + 128 * j);
+                mask |= (uint32_t)(v.x >= tf) << (4 * j);
+                mask |= (uint32_t)(v.y >= tf) << (4 * j + 1);
+                mask |= (uint32_t)(v.z >= tf) << (4 * j + 2);
+                mask |= (uint32_t)(v.w >= tf) << (4 * j + 3);
+            }
+        } else {
+            float4 v[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) v[j] = *reinterpret_cast<const float4*>(sp + tb + 128 * j);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const float m = fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w));
+                if (m >= tf) {
+                    mask |= (uint32_t)(v[j].x >= tf) << (4 * j);
+                    mask |= (uint32_t)(v[j].y >= tf) << (4 * j + 1);
+                    mask |= (uint32_t)(v[j].z >= tf) << (4 * j + 2);
+                    mask |= (uint32_t)(v[j].w >= tf) << (4 * j + 3);
+                }
+            }
+        }
+        const uint32_t cnt = __popc(mask);
+        const uint32_t incl = warp_incl(cnt, lane);
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        int b = 0;
+        if (lane == 31 && wtot) b = atomicAdd(misc, (int)wtot);
+        const int base = __shfl_sync(0xffffffffu, b, 31);
+        int pos = base + (int)(incl - cnt);
+        const int ibase = rd * RF + tb;
+        while (mask) {
+            const int e = 31 - __clz(mask);
+            mask ^= 1u << e;
+            const int off = ((e & ~3) << 5) | (e & 3);
+            const uint32_t u = __float_as_uint(sp[tb + off]);
+            const int p = pos & (CAP - 1);
+            bkey[p] = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+            bidx[p] = ibase + off;
+            ++pos;
+        }
+        __syncthreads();
+        if (tid == 0)
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int t = rd * R + q + NS;
+                if (t < ntiles) issue(smem_u32(ring + (s0 + q) * SF), x + (size_t)t * SF, SF * 4, smem_u32(full + s0 + q));
+            }
+    }
+    __syncthreads();
+    if (tid == 0) out_cnt[blockIdx.x] = misc[0];
+}
+
+__global__ void init_normal(float* d, size_t n)
+{
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    for (; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint64_t z = i * 0x9E3779B97F4A7C15ull + 12345;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const float u1 = ((z >> 40) + 1) * (1.0f / 16777217.0f), u2 = ((z & 0xffffff) + 0.5f) * (1.0f / 16777216.0f);
+        d[i] = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+    }
+}
+
+int main(int argc, char** argv)
+{
+    const int only = argc > 1 ? atoi(argv[1]) : -1;
+    const float tf = argc > 2 ? atof(argv[2]) : 1.645f;
+    int idx = 0;
+    const int n = 98304;
+    const int max_rows = 148 * 4;
+    float* d;
+    int* cnt;
+    cudaMalloc(&d, (size_t)max_rows * n * 4);
+    init_normal<<<1024, 256>>>(d, (size_t)max_rows * n);
+    cudaMalloc(&cnt, max_rows * 4);
+    float* flush;
+    cudaMalloc(&flush, 512 << 20);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto run = [&](const char* name, auto kern, int nt, int smem_need, int cps) {
+        if (only >= 0 && idx++ != only) return;
+        const int smem = 227 * 1024 / cps - 1024;
+        if (smem < smem_need) {
+            printf("%-44s %d/SM: does not fit (%d > %d)\n", name, cps, smem_need, smem);
+            return;
+        }
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        for (int rows : {148 * cps, 488}) {
+            float best = 1e9f;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaMemset(flush, rep, 512 << 20);
+                cudaEventRecord(e0);
+                kern<<<rows, nt, smem>>>(d, n, tf, cnt);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            int c0;
+            cudaMemcpy(&c0, cnt, 4, cudaMemcpyDeviceToHost);
+            printf("%-44s %d/SM rows %4d  %7.1f us  %7.1f GB/s  cnt0 %d %s\n", name, cps, rows, best * 1e3,
+                   (double)rows * n * 4 / 1e9 / (best * 1e-3), c0, cudaGetErrorString(cudaGetLastError()));
+        }
+    };
+#define RUN(NT, NS, SF, R, CAP, MODE, CPS)                                                                      \
+    run(#NT "thr " #NS "x" #SF " R" #R " cap" #CAP " m" #MODE, collect<NT, NS, SF, R, CAP, MODE>, NT,          \
+        NS * SF * 4 + CAP * 8 + NS * 8 + 64, CPS)
+    RUN(512, 3, 8192, 1, 8192, 0, 1);   // 0: previous best geometry, new loop
+    RUN(512, 4, 8192, 2, 8192, 0, 1);   // 1
+    RUN(512, 4, 8192, 2, 8192, 1, 1);   // 2
+    RUN(256, 4, 4096, 2, 8192, 0, 1);   // 3
+    RUN(256, 6, 4096, 2, 8192, 0, 1);   // 4
+    RUN(256, 4, 4096, 2, 4096, 0, 2);   // 5
+    RUN(256, 4, 2048, 2, 4096, 0, 2);   // 6
+    RUN(512, 4, 4096, 2, 4096, 0, 2);   // 7
+    RUN(512, 2, 8192, 2, 4096, 0, 2);   // 8
+    RUN(256, 4, 2048, 2, 4096, 0, 3);   // 9
+    RUN(256, 2, 4096, 2, 4096, 0, 3);   // 10
+    RUN(512, 4, 4096, 2, 8192, 0, 1);   // 11
+    RUN(1024, 4, 8192, 2, 8192, 0, 1);  // 12
+    RUN(1024, 2, 16384, 2, 8192, 0, 1); // 13
+    RUN(512, 6, 8192, 2, 4096, 0, 1);   // 14
+    RUN(256, 2, 4096, 2, 4096, 1, 3);   // 15
+    RUN(128, 4, 1024, 2, 4096, 0, 3);   // 16
+    return 0;
+}

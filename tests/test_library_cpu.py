@@ -36,7 +36,7 @@ def test_header_declares_the_boundary():
     names = _declared_functions()
     for required in ("gvr_topk_batched", "gvr_topk_batched_ex", "radix_topk_batched",
                      "radix_topk_batched_ex", "gvr_status_string", "gvr_topk_batched_host",
-                     "gvr_workspace_create", "gvr_workspace_destroy", "gvr_version"):
+                     "gvr_workspace_create", "gvr_workspace_destroy", "gvr_version", "gvr_kernel_info"):
         assert required in names
 
 
