@@ -105,10 +105,12 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
                                float* out_val, gvr_row_stats* stats);
 
 /* Per-phase timing of the GVR kernel (the paper's GVR_PHASE_TIMING instrumentation,
- * PAPER.md:1645-1656): phase_ts is a device int64 [num_rows, 6] array receiving clock64()
- * of each row's CTA at: start, end of Phase 1, end of the streaming pass, end of Phases
- * 2-3, end of Phase 4, end.  Rows that take a fallback or the len <= k path leave the
- * intermediate stamps 0.  Same result as gvr_topk_batched (prev_topk nullable). */
+ * PAPER.md:1645-1656): phase_ts is a device int64 [num_rows, 9] array receiving clock64()
+ * of each row's CTA at: start, end of Phase 1 (the guess hand-off read), end of the
+ * streaming pass, end of Phases 2-3, end of Phase 4, end; then %globaltimer (ns) at the
+ * CTA's start and end, and the SM id (%smid) the CTA ran on.  Rows that take a fallback
+ * or the len <= k path leave the intermediate clock64 stamps 0.  Same result as
+ * gvr_topk_batched (prev_topk nullable). */
 gvr_status gvr_topk_phase_timing(const float* scores, int64_t row_stride, const int32_t* row_lens,
                                  int32_t num_rows, const int32_t* prev_topk, int32_t k, int32_t* out_idx,
                                  cudaStream_t stream, long long* phase_ts);

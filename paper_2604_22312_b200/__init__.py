@@ -160,11 +160,12 @@ PHASES = ("phase1", "stream", "phase2_3", "phase4", "output")
 
 
 def topk_phase_timing(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None):
-    """GVR Top-K plus per-row clock64 stamps [R, 6] (start, end of Phase 1, stream,
-    Phases 2-3, Phase 4, end) — the paper's per-phase breakdown (Table 8)."""
+    """GVR Top-K plus per-row stamps [R, 9]: clock64 at start, end of Phase 1, stream,
+    Phases 2-3, Phase 4, end — the paper's per-phase breakdown (Table 8) — then the
+    global timer (ns) at the CTA's start and end and the SM id."""
     torch = _torch()
     R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
-    ts = torch.zeros((R, 6), dtype=torch.int64, device=scores.device)
+    ts = torch.zeros((R, 9), dtype=torch.int64, device=scores.device)
     _check(_load().gvr_topk_phase_timing(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
                                          _ptr(out), _stream_ptr(stream), _ptr(ts)))
     return out, ts

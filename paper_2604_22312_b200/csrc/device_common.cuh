@@ -23,8 +23,8 @@ constexpr int CHUNK_SLOTS = 8;          // buffer slots per thread per compactio
 constexpr int NCHUNK_MAX = 4;           // chunks per count cache (capacity <= 4 * 8 * group size)
 constexpr int VEC = 4;                  // float4 loads per thread per register tile
 constexpr int SORT_MAX = 4096;          // largest bitonic ordered-output sort (64-bit composites)
-constexpr int CSORT_BIN_MAX = 32;       // counting sort: largest bin ranked in place
-constexpr int LIST_MAX = 2048;          // Phase 4: largest K-th-bin member list
+constexpr int CSORT_BIN_MAX = 256;      // counting sort: largest bin ranked in place
+constexpr int LIST_MAX = 64;            // Phase 4: largest K-th-bin snapped over (else narrowed)
 constexpr int RADIX_EARLY = 2048;       // radix early exit
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -124,7 +124,7 @@ struct Work {
     __device__ __forceinline__ uint32_t* list() const { return reinterpret_cast<uint32_t*>(aux); }
 };
 __host__ __device__ constexpr int work_bytes(int csort_cap) { return 2 * NBINS * 4 + csort_cap * 8; }
-static_assert(LIST_MAX * 4 <= NBINS * 4 + KMAX * 8, "list fits aux + csort");
+static_assert(LIST_MAX * 4 <= NBINS * 4, "list fits aux");
 
 // ---------------------------------------------------------------------------------
 // Group reductions.

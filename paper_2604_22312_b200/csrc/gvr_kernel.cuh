@@ -5,8 +5,8 @@
 //
 // Method: PAPER.md Sec. 4 (lines 379-690).  Per row:
 //   Phase 1 (Guess): x at the previous step's Top-K positions ->
-//     pmin / pmax / pmean (Eq. 4) plus the second moment; T_c = pmean - sigma*sd.  The
-//     TMA ring is primed first, so the first 64 KB of the row load during Phase 1.
+//     pmin / pmax / pmean (Eq. 4) plus the second moment; T_c = pmean - sigma*sd.  Runs
+//     as a separate short kernel (gvr_guess_kernel) ahead of the streaming kernel.
 //   Streaming pass (B200 re-design of the Phase-2 count pass fused with the Phase-3
 //     collector): the row body is read from HBM exactly once, in
 //     rounds of 2 x 16 KB TMA tiles; every element whose key is >= T_c is appended to
@@ -42,7 +42,7 @@ struct GvrParams {
 constexpr int GVR_NT = 256;
 constexpr int GVR_CAP = 6016;   // candidate buffer capacity (C = 6144 less the raise histogram)
 constexpr int RAISE_BINS = 256;  // raise_threshold histogram (one bin per thread)
-constexpr int GVR_CSORT = KMAX;  // counting-sort capacity
+constexpr int GVR_CSORT = SORT_MAX;  // counting-sort capacity (K plus ties at T*)
 using GvrGroup = Group<GVR_NT, 1>;
 
 // Shared-memory layout (dynamic).  The refine work area aliases the ring, which is idle
@@ -63,7 +63,28 @@ static_assert(RAISE_BINS == GVR_NT, "one raise bin per thread");
 
 // Phase timestamps (written when phase_ts != nullptr): the paper's GVR_PHASE_TIMING
 // instrumentation.
-enum { TS_START = 0, TS_PHASE1, TS_STREAM, TS_PHASE23, TS_PHASE4, TS_END, TS_N };
+enum { TS_START = 0, TS_PHASE1, TS_STREAM, TS_PHASE23, TS_PHASE4, TS_END, TS_GSTART, TS_GEND, TS_SMID, TS_N };
+
+__device__ __forceinline__ long long global_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return (long long)t;
+}
+__device__ __forceinline__ long long sm_id()
+{
+    uint32_t s;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+    return (long long)s;
+}
+
+// What Phase 1 (gvr_guess_kernel) hands to the streaming kernel, per row.
+struct GuessOut {
+    uint32_t Tc;    // collect threshold key
+    uint32_t T0;    // f2key(pmean), the Phase-2 start
+    int32_t t0_ok;  // pmean finite
+    int32_t pad;
+};
 
 // What the streaming pass hands to Phases 2-4.
 struct RowMeta {
@@ -500,12 +521,120 @@ __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work
 }
 
 
+// ---------------- Phase 1: guess statistics (Eq. 4)
+// x at the previous step's Top-K positions -> pmin / pmax / pmean plus the second
+// moment; T_c = pmean - sigma * sd (R5), T0 = pmean for Phase 2.  Runs as its
+// own kernel ahead of the streaming kernel: with every row's gathers in flight at once
+// and no streaming traffic in the memory queues, the two dependent round trips (guess
+// indices, then the values) cost one short kernel instead of stalling each row's CTA.
+constexpr int GUESS_NT = 256;
+using GuessGroup = Group<GUESS_NT, 1>;
+
+//
+// It also schedules the streaming kernel: a strided sample of GUESS_NT row values
+// estimates f(T_c); rows whose estimate exceeds the buffer (poor guesses, which need
+// threshold raises) are put at the front of the row order, the others at the back, so
+// the expensive rows start in the first wave instead of setting the makespan.
+struct RowSched {
+    int32_t* order;    // [num_rows]: CTA b of the streaming kernel processes row order[b]
+    int32_t* cursors;  // [2]: front / back fill counts, zeroed before the launch
+};
+
+__global__ void __launch_bounds__(GUESS_NT)
+gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens,
+                 const int32_t* prev, int k, int num_rows, GvrParams prm, GuessOut* __restrict__ gp, RowSched sched)
+{
+    __shared__ __align__(16) unsigned char scratch[GROUP_SCRATCH_BYTES];
+    GuessGroup c;
+    c.init(threadIdx.x, scratch);
+    const int r = blockIdx.x;
+    const RowPlan p = plan_row(scores, stride, row_lens, r, k);
+    if (p.n <= k) {  // trivial row: no guess needed (block-uniform); scheduled last
+        if (c.tid == 0) sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
+        return;
+    }
+    // one strided row sample per thread, gathered alongside the guess values
+    const float xs = __ldg(p.x + (int)(((int64_t)c.tid * p.n) / GUESS_NT));
+    constexpr int GPT = KMAX / GUESS_NT;  // 8 guesses per thread
+    const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
+    float gv[GPT];
+    uint32_t valid = 0;
+    if (pr) {
+        int32_t gi[GPT];
+#pragma unroll
+        for (int j = 0; j < GPT; ++j) {
+            const int q = c.tid + j * GUESS_NT;
+            gi[j] = q < k ? __ldg(pr + q) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < GPT; ++j) {
+            gv[j] = 0.f;
+            if (gi[j] >= 0 && gi[j] < p.n) {
+                gv[j] = __ldg(p.x + gi[j]);
+                valid |= 1u << j;
+            }
+        }
+    }
+    uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
+    float sum = 0.f, sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < GPT; ++j) {
+        if ((valid >> j) & 1u) {
+            const uint32_t kv = f2key(gv[j]);
+            kmn = min(kmn, kv);
+            kmx = max(kmx, kv);
+            ++cnt;
+            sum += gv[j];
+            sq += gv[j] * gv[j];
+        }
+    }
+    group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+    if (cnt == 0) {
+        // no valid guess: deterministic stride sample of M values
+        kmn = 0xffffffffu;
+        kmx = 0u;
+        sum = sq = 0.f;
+        const int M = min(KMAX, p.n);
+        for (int j = c.tid; j < M; j += GUESS_NT) {
+            const int q = (int)(((int64_t)j * p.n) / M);
+            const float v = __ldg(p.x + q);
+            const uint32_t kv = f2key(v);
+            kmn = min(kmn, kv);
+            kmx = max(kmx, kv);
+            ++cnt;
+            sum += v;
+            sq += v * v;
+        }
+        group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+    }
+    group_fsum2(c, sum, sq);
+    const float pmean = sum / (float)cnt;
+    const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
+    const float tcf = pmean - prm.collect_sigma * sqrtf(var);
+    GuessOut g;
+    g.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
+    if (p.n <= GVR_CAP) g.Tc = 0u;  // the whole row fits in B
+    g.T0 = f2key(pmean);
+    g.t0_ok = isfinite(pmean) ? 1 : 0;
+    g.pad = 0;
+    const uint32_t hits = group_red1<R_ADD>(c, f2key(xs) >= g.Tc ? 1u : 0u);
+    if (c.tid == 0) {
+        gp[r] = g;
+        const bool heavy = (double)hits * p.n > (double)GVR_CAP * GUESS_NT;  // estimated f(T_c) > capacity
+        if (heavy)
+            sched.order[atomicAdd(sched.cursors, 1)] = r;
+        else
+            sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
+    }
+}
+
 __global__ void __launch_bounds__(GVR_NT, 2)
-gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, const int32_t* prev,
-                int k, int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, long long* phase_ts)
+gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
+                int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
+                const int32_t* __restrict__ order, long long* phase_ts)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int r = blockIdx.x;
+    const int r = __ldg(order + blockIdx.x);
     const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
                     policy_evict_first()};
     const Buf B{reinterpret_cast<uint32_t*>(smem + G_OFF_B), reinterpret_cast<int32_t*>(smem + G_OFF_B + GVR_CAP * 4),
@@ -527,75 +656,19 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
     float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
     int st[4] = {0, 0, 0, 0};
     int done_kind = GVR_DONE_CONVERGED, passes = 1, raises = 0, ftc_stat = 0;
-    long long tsr[TS_N] = {ts0, 0, 0, 0, 0, 0};
+    long long tsr[TS_N] = {ts0, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
     if (p.n <= k) {
         c.sync();
         small_row_emit(c, B, Wk, g, k, o, ov);
         done_kind = GVR_DONE_TRIVIAL;
         st[2] = p.n;
     } else {
-        // ---------------- Phase 1: guess statistics (Eq. 4)
-        constexpr int GPT = KMAX / GVR_NT;  // 8 guesses per thread
-        const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
-        float gv[GPT];
-        uint32_t valid = 0;
-        if (pr) {
-            int32_t gi[GPT];
-#pragma unroll
-            for (int j = 0; j < GPT; ++j) {
-                const int q = c.tid + j * GVR_NT;
-                gi[j] = q < k ? __ldg(pr + q) : -1;
-            }
-#pragma unroll
-            for (int j = 0; j < GPT; ++j) {
-                gv[j] = 0.f;
-                if (gi[j] >= 0 && gi[j] < p.n) {
-                    gv[j] = __ldg(p.x + gi[j]);
-                    valid |= 1u << j;
-                }
-            }
-        }
-        uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
-        float sum = 0.f, sq = 0.f;
-#pragma unroll
-        for (int j = 0; j < GPT; ++j) {
-            if ((valid >> j) & 1u) {
-                const uint32_t kv = f2key(gv[j]);
-                kmn = min(kmn, kv);
-                kmx = max(kmx, kv);
-                ++cnt;
-                sum += gv[j];
-                sq += gv[j] * gv[j];
-            }
-        }
-        group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);  // (also publishes the barrier init)
-        if (cnt == 0) {
-            // no valid guess: deterministic stride sample of M values
-            kmn = 0xffffffffu;
-            kmx = 0u;
-            sum = sq = 0.f;
-            const int M = min(KMAX, p.n);
-            for (int j = c.tid; j < M; j += GVR_NT) {
-                const int q = (int)(((int64_t)j * p.n) / M);
-                const float v = __ldg(p.x + q);
-                const uint32_t kv = f2key(v);
-                kmn = min(kmn, kv);
-                kmx = max(kmx, kv);
-                ++cnt;
-                sum += v;
-                sq += v * v;
-            }
-            group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
-        }
-        group_fsum2(c, sum, sq);
-        const float pmean = sum / (float)cnt;
-        const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
-        const float tcf = pmean - prm.collect_sigma * sqrtf(var);
+        // ---------------- Phase 1 ran in gvr_guess_kernel
+        const GuessOut gq = gp[r];
         RowMeta m;
-        m.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
-        if (p.n <= B.cap) m.Tc = 0u;  // the whole row fits in B
-        m.T0 = f2key(pmean);
-        m.t0_ok = isfinite(pmean);
+        m.Tc = gq.Tc;
+        m.T0 = gq.T0;
+        m.t0_ok = gq.t0_ok != 0;
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         // ---------------- streaming pass (HBM read once, TMA ring)
         uint32_t kmax = 0u, extras = 0u;
@@ -639,6 +712,8 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         }
         if (phase_ts) {
             tsr[TS_END] = clock64();
+            tsr[TS_GEND] = global_ns();
+            tsr[TS_SMID] = sm_id();
             for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = tsr[i];
         }
     }

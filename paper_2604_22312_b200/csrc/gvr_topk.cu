@@ -107,10 +107,35 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
     }
     if ((st = set_smem(gvr_topk_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;
-    // one CTA per row, two CTAs per SM
-    gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, prev_topk, k, out_idx,
-                                                                  out_val, stats, prm, phase_ts);
-    return launch_status();
+    // Phase 1 for every row (one small CTA per row), then the streaming / refine kernel
+    // (one CTA per row, two CTAs per SM).  The per-row hand-off lives in stream-ordered
+    // pool memory, so concurrent calls on different streams do not share scratch.
+    // scratch: GuessOut[num_rows] | order[num_rows] | cursors[2]
+    const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
+    const size_t scratch_bytes = gp_bytes + (size_t)num_rows * 4 + 8;
+    unsigned char* scratch = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, stream) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    GuessOut* gp = reinterpret_cast<GuessOut*>(scratch);
+    RowSched sched{reinterpret_cast<int32_t*>(scratch + gp_bytes),
+                   reinterpret_cast<int32_t*>(scratch + gp_bytes + (size_t)num_rows * 4)};
+    if (cudaMemsetAsync(sched.cursors, 0, 8, stream) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        (void)cudaFreeAsync(scratch, stream);
+        return GVR_ERR_CUDA;
+    }
+    gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm, gp,
+                                                        sched);
+    gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
+                                                                  stats, prm, gp, sched.order, phase_ts);
+    const gvr_status ls = launch_status();
+    if (cudaFreeAsync(scratch, stream) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    return ls;
 }
 
 gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
