@@ -81,9 +81,16 @@ def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0):
 
 
 def algorithmic_bytes(lens, k=K):
-    """Bytes the method must move per launch: each row read once (4N), the guess read
+    """Bytes the method must move per call: each row read once (4N), the guess read
     (4K), the output written (4K) and the row length (4) — SURVEY.md 8(d) B(N)."""
     return int(4 * int(np.sum(lens)) + len(lens) * (4 * k + 4 * k + 4))
+
+
+def stream_kernel_bytes(lens, k=K):
+    """Algorithmic bytes of the streaming / refine kernel alone (gvr_topk_kernel): the
+    row read once (4N), the output written (4K) and the row length (4); the guess read
+    and its gathers belong to gvr_guess_kernel."""
+    return int(4 * int(np.sum(lens)) + len(lens) * (4 * k + 4))
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -153,20 +160,36 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- timing
-def time_steps(fn, batches, steps, warmup, stream, sampler=None):
+KERNEL_EVENT_EVERY = 4  # per-kernel events on every 4th timed step (each record costs ~2-3 us)
+
+
+def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=False):
+    """Device time of `steps` calls (seconds).  With kernel_events, every
+    KERNEL_EVENT_EVERY-th call is fn(batch, evs), which also records per-kernel events on
+    the launch stream; the mean per-kernel times (seconds per launch) are returned too."""
     import torch
     for i in range(warmup):
         fn(batches[i % len(batches)])
     torch.cuda.synchronize()
+    sampled = [i for i in range(steps) if i % KERNEL_EVENT_EVERY == 0] if kernel_events else []
+    evs = {i: [torch.cuda.Event(enable_timing=True) for _ in range(3)] for i in sampled}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for i in range(steps):
-        fn(batches[i % len(batches)])
+        if i in evs:
+            fn(batches[i % len(batches)], evs[i])
+        else:
+            fn(batches[i % len(batches)])
     ev1.record(stream)
     if sampler is not None:
         sampler.sample_now()  # GPU still executing the queued steps
     torch.cuda.synchronize()
-    return ev0.elapsed_time(ev1) / 1e3  # seconds
+    total = ev0.elapsed_time(ev1) / 1e3
+    if not kernel_events:
+        return total
+    guess = sum(e[0].elapsed_time(e[1]) for e in evs.values()) / 1e3 / len(evs)
+    main = sum(e[1].elapsed_time(e[2]) for e in evs.values()) / 1e3 / len(evs)
+    return total, {"gvr_guess_kernel": guess, "gvr_topk_kernel": main, "sampled_steps": len(evs)}
 
 
 def cpu_oracle_rate(host_scores, lens, max_rows=None, threads=None):
@@ -227,8 +250,11 @@ def main():
     for b in batches:
         b["out"] = torch.empty((R, K), dtype=torch.int32, device=dev)
 
-    def gvr_step(b):
-        gvr.topk(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"])
+    def gvr_step(b, evs=None):
+        if evs is None:
+            gvr.topk(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"])
+        else:
+            gvr.topk_events(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"], events=evs)
 
     def radix_step(b):
         gvr.radix_topk(b["scores"], K, row_lens=b["row_lens"], out=b["out"])
@@ -257,8 +283,13 @@ def main():
     torch.cuda.synchronize()
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     phys = vis.split(",")[local_rank] if vis else str(local_rank)
+    kern_times = None
     with ClockSampler(phys) as clk:
-        elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk)
+        if args.impl == "gvr":
+            elapsed, kern_times = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk,
+                                             kernel_events=True)
+        else:
+            elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk)
     if dist is not None:
         t = torch.tensor([elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -293,8 +324,15 @@ def main():
         peak = float(peaks.get("hbm_gbs", 6650.0))
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
         abytes = algorithmic_bytes(lens_np)
-        kern_s = elapsed / args.steps  # one launch per step
-        achieved = abytes / kern_s / 1e9
+        step_gbs = abytes / (elapsed / args.steps) / 1e9  # whole call (all kernels + gaps)
+        if args.impl == "gvr":
+            # dominant kernel: the streaming / refine kernel, timed by its own events
+            kbytes = stream_kernel_bytes(lens_np)
+            kern_s = kern_times["gvr_topk_kernel"]
+        else:
+            kbytes = abytes  # the radix kernel is the whole call
+            kern_s = elapsed / args.steps
+        achieved = kbytes / kern_s / 1e9
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tf):
@@ -325,15 +363,19 @@ def main():
             "us_per_row": round(elapsed / (R * args.steps) * 1e6, 5),
             "speedup_vs_radix": round(rad_t / gvr_t, 3),
             "radix_rows_per_s": round(R * world * args.steps / rad_t, 1),
-            "hbm_gbs": round(achieved, 1),
+            "hbm_gbs": round(step_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "peak_source": peak_src, "algorithmic_bytes_per_launch": abytes,
-                         "kernel": "gvr_topk_kernel" if args.impl == "gvr" else "radix_topk_kernel"},
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes,
+                         "kernel": "gvr_topk_kernel" if args.impl == "gvr" else "radix_topk_kernel",
+                         "kernel_us_per_launch": round(kern_s * 1e6, 2),
+                         "step_gbs": round(step_gbs, 1)},
+            "kernel_us_per_launch": ({k: round(kern_times[k] * 1e6, 2) for k in ("gvr_guess_kernel", "gvr_topk_kernel")}
+                                     | {"sampled_steps": kern_times["sampled_steps"]} if kern_times else None),
             "passes_per_row": {"global_mean": float(st[:, 4].mean()), "secant_mean": float(st[:, 0].mean()),
                                "snap_mean": float(st[:, 1].mean()), "raises_mean": float(st[:, 5].mean()),
                                "cand_mean": float(st[:, 2].mean())},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (2 if args.impl == "gvr" else 1),
             "clocks": clk.summary(),
             "check": check,
         }

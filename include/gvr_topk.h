@@ -104,6 +104,17 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
                                int32_t* out_idx, cudaStream_t stream, const gvr_options* opt,
                                float* out_val, gvr_row_stats* stats);
 
+/* Same as gvr_topk_batched, and records caller-created CUDA events (cudaEventCreate;
+ * any may be NULL) on `stream` right before the Phase-1 guess kernel (guess_start),
+ * between it and the streaming / refine kernel (stream_start), and after that kernel
+ * (stream_end), so the caller can time each kernel of the call with
+ * cudaEventElapsedTime (the benchmark's per-kernel roofline).  Ownership of the events
+ * stays with the caller. */
+gvr_status gvr_topk_batched_events(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                                   int32_t num_rows, const int32_t* prev_topk, int32_t k, int32_t* out_idx,
+                                   cudaStream_t stream, cudaEvent_t guess_start, cudaEvent_t stream_start,
+                                   cudaEvent_t stream_end);
+
 /* Per-phase timing of the GVR kernel (the paper's GVR_PHASE_TIMING instrumentation,
  * PAPER.md:1645-1656): phase_ts is a device int64 [num_rows, 9] array receiving clock64()
  * of each row's CTA at: start, end of Phase 1 (the guess hand-off read), end of the

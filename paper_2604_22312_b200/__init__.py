@@ -58,6 +58,7 @@ def _load():
         "gvr_workspace_destroy": [vp],
         "gvr_topk_batched_host": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
         "gvr_topk_phase_timing": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
+        "gvr_topk_batched_events": [vp, i64, vp, i32, vp, i32, vp, vp, vp, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -157,6 +158,24 @@ def topk_ex(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, values: 
 
 
 PHASES = ("phase1", "stream", "phase2_3", "phase4", "output")
+
+
+def topk_events(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, events=(None, None, None),
+                stream=None):
+    """gvr.topk that also records three torch.cuda.Events (each may be None) before the
+    guess kernel, between the two kernels and after the streaming kernel."""
+    R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
+    hs = []
+    for e in events:
+        if e is None:
+            hs.append(None)
+        else:
+            if e.cuda_event == 0:  # created lazily by torch: force creation
+                e.record()
+            hs.append(ctypes.c_void_p(e.cuda_event))
+    _check(_load().gvr_topk_batched_events(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k, _ptr(out),
+                                           _stream_ptr(stream), *hs))
+    return out
 
 
 def topk_phase_timing(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None):

@@ -1,5 +1,6 @@
 // gvr_topk.cu — C ABI of libgvrtopk.so (declared in include/gvr_topk.h): argument
 // validation, launch configuration and the host-buffer workspace entry point.
+#include <mutex>
 #include <type_traits>
 
 #include "../../include/gvr_topk.h"
@@ -28,6 +29,30 @@ gvr_status validate(const float* scores, int64_t row_stride, int32_t num_rows, i
     if (row_stride > 0x7fffffffLL) return GVR_ERR_UNSUPPORTED;
     if (num_rows > 0 && (scores == nullptr || out == nullptr)) return GVR_ERR_INVALID_ARGUMENT;
     return GVR_OK;
+}
+
+// Stream-ordered scratch for the guess-kernel hand-off: a private memory pool per device
+// that never trims (release threshold = max), so steady-state calls reuse the same pages
+// instead of re-mapping them after every synchronisation, as the default pool would.
+cudaMemPool_t scratch_pool()
+{
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+        unsigned long long thr = ~0ull;
+        (void)cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = p;
+    }
+    return pools[dev];
 }
 
 template <class Kern>
@@ -91,7 +116,8 @@ const char* gvr_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_er
 
 static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
                              const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
-                             const gvr_options* opt, float* out_val, gvr_row_stats* stats, long long* phase_ts)
+                             const gvr_options* opt, float* out_val, gvr_row_stats* stats, long long* phase_ts,
+                             cudaEvent_t const* ev = nullptr)
 {
     gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
     if (st != GVR_OK) return st;
@@ -114,7 +140,8 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
     const size_t scratch_bytes = gp_bytes + (size_t)num_rows * 4 + 8;
     unsigned char* scratch = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, stream) != cudaSuccess) {
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool || cudaMallocFromPoolAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, pool, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
@@ -126,10 +153,16 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         (void)cudaFreeAsync(scratch, stream);
         return GVR_ERR_CUDA;
     }
+    auto mark = [&](int i) {
+        if (ev && ev[i]) (void)cudaEventRecord(ev[i], stream);
+    };
+    mark(0);
     gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm, gp,
                                                         sched);
+    mark(1);
     gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
                                                                   stats, prm, gp, sched.order, phase_ts);
+    mark(2);
     const gvr_status ls = launch_status();
     if (cudaFreeAsync(scratch, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
@@ -144,6 +177,16 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
 {
     return gvr_launch(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, opt, out_val, stats,
                       nullptr);
+}
+
+gvr_status gvr_topk_batched_events(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                                   int32_t num_rows, const int32_t* prev_topk, int32_t k, int32_t* out_idx,
+                                   cudaStream_t stream, cudaEvent_t guess_start, cudaEvent_t stream_start,
+                                   cudaEvent_t stream_end)
+{
+    const cudaEvent_t ev[3] = {guess_start, stream_start, stream_end};
+    return gvr_launch(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, nullptr, nullptr, nullptr,
+                      nullptr, ev);
 }
 
 gvr_status gvr_topk_phase_timing(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
