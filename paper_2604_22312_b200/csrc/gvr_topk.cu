@@ -1,6 +1,8 @@
 // gvr_topk.cu — C ABI of libgvrtopk.so (declared in include/gvr_topk.h): argument
 // validation, launch configuration and the host-buffer workspace entry point.
+#include <map>
 #include <mutex>
+#include <utility>
 #include <type_traits>
 
 #include "../../include/gvr_topk.h"
@@ -53,6 +55,46 @@ cudaMemPool_t scratch_pool()
         pools[dev] = p;
     }
     return pools[dev];
+}
+
+// Per-(device, stream) scratch for the guess-kernel hand-off, grown stream-ordered
+// from scratch_pool() and then reused: steady-state calls allocate nothing (CUDA-Graph
+// friendly).  Calls on one stream are serialised by the stream, so one buffer per
+// stream is race-free.  While the stream is being captured the cache is not modified:
+// a too-small cache is bypassed with an allocation / free pair recorded in the graph.
+struct ScratchLease {
+    unsigned char* ptr = nullptr;
+    bool temporary = false;  // free after the launch (capture-time allocation)
+};
+
+cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lease)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool) return cudaErrorMemoryAllocation;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(stream, &cap)) != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& slot = cache[std::make_pair(dev, stream)];
+    if (slot.second >= bytes) {
+        lease.ptr = static_cast<unsigned char*>(slot.first);
+        return cudaSuccess;
+    }
+    if (cap != cudaStreamCaptureStatusNone) {
+        lease.temporary = true;
+        return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&lease.ptr), bytes, pool, stream);
+    }
+    const size_t grow = bytes > 2 * slot.second ? bytes : 2 * slot.second;
+    void* p = nullptr;
+    if ((e = cudaMallocFromPoolAsync(&p, grow, pool, stream)) != cudaSuccess) return e;
+    if (slot.first) (void)cudaFreeAsync(slot.first, stream);  // stream-ordered after earlier users
+    slot = std::make_pair(p, grow);
+    lease.ptr = static_cast<unsigned char*>(p);
+    return cudaSuccess;
 }
 
 template <class Kern>
@@ -134,23 +176,24 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     }
     if ((st = set_smem(gvr_topk_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;
     // Phase 1 for every row (one small CTA per row), then the streaming / refine kernel
-    // (one CTA per row, two CTAs per SM).  The per-row hand-off lives in stream-ordered
-    // pool memory, so concurrent calls on different streams do not share scratch.
+    // (one CTA per row, two CTAs per SM).  The per-row hand-off lives in the stream's
+    // cached scratch (acquire_scratch), so concurrent calls on different streams do not
+    // share it and steady-state calls allocate nothing.
     // scratch: GuessOut[num_rows] | order[num_rows] | cursors[2]
     const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
     const size_t scratch_bytes = gp_bytes + (size_t)num_rows * 4 + 8;
-    unsigned char* scratch = nullptr;
-    cudaMemPool_t pool = scratch_pool();
-    if (!pool || cudaMallocFromPoolAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, pool, stream) != cudaSuccess) {
+    ScratchLease lease;
+    if (acquire_scratch(stream, scratch_bytes, lease) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
+    unsigned char* scratch = lease.ptr;
     GuessOut* gp = reinterpret_cast<GuessOut*>(scratch);
     RowSched sched{reinterpret_cast<int32_t*>(scratch + gp_bytes),
                    reinterpret_cast<int32_t*>(scratch + gp_bytes + (size_t)num_rows * 4)};
     if (cudaMemsetAsync(sched.cursors, 0, 8, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
-        (void)cudaFreeAsync(scratch, stream);
+        if (lease.temporary) (void)cudaFreeAsync(scratch, stream);
         return GVR_ERR_CUDA;
     }
     auto mark = [&](int i) {
@@ -164,7 +207,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
                                                                   stats, prm, gp, sched.order, phase_ts);
     mark(2);
     const gvr_status ls = launch_status();
-    if (cudaFreeAsync(scratch, stream) != cudaSuccess) {
+    if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
