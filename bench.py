@@ -10,9 +10,17 @@ scores (Eq. 1, synthetic, prev-step guesses), K = 2048.  Inputs are res
 in HBM before the timed region; three distinct batches are rotated so every step reads
 cold data (3 x 195 MB > 126 MB L2).  Rank 0 prints one JSON line.
 
+A step launches two kernels of ours (gvr_guess_kernel: Phase 1 for every row, then
+gvr_topk_kernel: stream + Phases 2-4 + ordered output); the roofline entry is for the
+dominant one (gvr_topk_kernel), timed by CUDA events recorded on its stream through
+gvr_topk_batched_events on every 4th timed step.
+
 Under torchrun (N > 1) every rank processes its own batch of the same shape (rows are
 independent; no collective on the hot path) — weak scaling; the elapsed time is the
-max over ranks.  --impl reference times the CPU oracle on the host (rank 0 only).
+max over ranks.  cfg5 instead splits one fixed 64 x 61 batch across the ranks
+(paper_2604_22312_b200.shard.row_partition) — strong scaling.  --gather also times the
+optional NCCL all-gather of out_idx, reported separately.  --impl reference times the
+CPU oracle on the host (rank 0 only).
 """
 from __future__ import annotations
 
@@ -36,7 +44,8 @@ CONFIGS = {
     "cfg2": dict(requests=8, layers=61, n=100_000, draft=1, desc="batch 8 x 61 layers, N=100K"),
     "cfg3": dict(requests=1, layers=1, n=131_072, draft=1, desc="batch-1 long context"),
     "cfg4": dict(requests=16, layers=61, n=100_000, draft=4, desc="MTP-3: 16 requests x 4 tokens x 61 layers"),
-    "cfg5": dict(requests=64, layers=61, n=131_072, draft=1, desc="64 requests x 61 layers, N=128K"),
+    "cfg5": dict(requests=64, layers=61, n=131_072, draft=1, split=True,
+                 desc="64 requests x 61 layers, N=128K, rows split across the GPUs"),
 }
 REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -50,30 +59,35 @@ def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0):
     Eq. 1 indexer (synth.IndexerLayer), plus prev_topk = the exact Top-K of the
     request's previous step (n - 1 keys), shared by its draft rows.
     The previous step's Top-K is computed with the GVR kernel itself (no guess), i.e.
-    the decode loop feeding its own output back; it is only a hint."""
+    the decode loop feeding its own output back; it is only a hint.
+    `requests` is a count (requests 0..count-1) or an explicit list of global request
+    ids (a rank's share of a split batch); `rank` enters the seed (weak scaling: every
+    rank its own rows)."""
     import torch
 
     import paper_2604_22312_b200 as gvr
     import synth
 
-    R = requests * layers * draft
+    req_ids = list(range(requests)) if isinstance(requests, int) else list(requests)
+    nreq = len(req_ids)
+    R = nreq * layers * draft
     S = n + draft - 1
     scores = torch.zeros((R, S), dtype=torch.float32, device=dev)
     lens = torch.empty(R, dtype=torch.int32)
-    prev_rows = torch.zeros((requests * layers, S), dtype=torch.float32, device=dev)
+    prev_rows = torch.zeros((nreq * layers, S), dtype=torch.float32, device=dev)
     row = 0
-    for q in range(requests):
+    for qi, q in enumerate(req_ids):
         for l in range(layers):
             s = synth.splitmix64(seed, rank, q, l)
             lay = synth.IndexerLayer(S, synth.layer_rho(l, seed), s, dev)
-            prev_rows[q * layers + l, :n - 1] = lay.scores(n - 1)
+            prev_rows[qi * layers + l, :n - 1] = lay.scores(n - 1)
             lay.step()
             for j in range(draft):
                 scores[row, :n + j] = lay.scores(n + j)
                 lens[row] = n + j
                 row += 1
             del lay
-    plens = torch.full((requests * layers,), n - 1, dtype=torch.int32, device=dev)
+    plens = torch.full((nreq * layers,), n - 1, dtype=torch.int32, device=dev)
     ptop = gvr.topk(prev_rows, K, row_lens=plens)
     prev = ptop.repeat_interleave(draft, dim=0).contiguous()
     del prev_rows
@@ -215,6 +229,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="verify every batch against the oracle")
+    ap.add_argument("--gather", action="store_true",
+                    help="N > 1: also time the optional NCCL all-gather of out_idx (reported separately)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -240,8 +256,17 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    batches = [make_decode_batch(cfg["requests"], cfg["layers"], cfg["n"], dev,
-                                 seed=synth.splitmix64(synth.BASE_SEED, b), draft=cfg["draft"], rank=rank)
+    split = bool(cfg.get("split"))
+    if split:
+        # strong scaling: the global batch is fixed, each rank owns a contiguous block of
+        # requests (equal rows, so the row_partition is by request)
+        from paper_2604_22312_b200.shard import row_partition
+        qb = row_partition(np.full(cfg["requests"], cfg["n"]), world)
+        reqs, seed_rank = list(range(int(qb[rank]), int(qb[rank + 1]))), 0
+    else:
+        reqs, seed_rank = cfg["requests"], rank
+    batches = [make_decode_batch(reqs, cfg["layers"], cfg["n"], dev,
+                                 seed=synth.splitmix64(synth.BASE_SEED, b), draft=cfg["draft"], rank=seed_rank)
                for b in range(args.nbatches)]
     torch.cuda.synchronize()
     R = batches[0]["R"]
@@ -296,7 +321,12 @@ def main():
         elapsed = float(t.item())
         dist.barrier()
     ms_per_step = elapsed / args.steps * 1e3
-    rows_total = R * world * args.steps
+    rows_all = R
+    if dist is not None:
+        t = torch.tensor([R], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        rows_all = int(t.item())
+    rows_total = rows_all * args.steps
     value = rows_total / elapsed
 
     # the other kernel, same protocol (speedup vs own radix select)
@@ -305,6 +335,28 @@ def main():
         t = torch.tensor([other_elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         other_elapsed = float(t.item())
+
+    # optional all-gather of every rank's indices (off the hot path, timed separately)
+    gather_info = None
+    if dist is not None and args.gather:
+        from paper_2604_22312_b200.shard import gather_rows
+        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([R], dtype=torch.int64, device=dev))
+        bounds = np.concatenate([[0], np.cumsum([int(x.item()) for x in sizes])])
+        for _ in range(3):
+            gather_rows(batches[0]["out"], bounds)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(10):
+            full = gather_rows(batches[0]["out"], bounds)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([g0.elapsed_time(g1) / 10 * 1e3], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather_info = {"allgather_us": round(float(t.item()), 2), "bytes_out": int(full.numel() * 4),
+                       "collective": "torch.distributed.all_gather (NCCL)"}
 
     # per-row stats (passes etc.) on one batch, outside the timed region
     b0 = batches[0]
@@ -351,7 +403,7 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if split else "weak",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (PAPER.md Eq. 1 indexer rows, YaRN RoPE, AR(1) decode steps; prev-step Top-K guesses)",
@@ -362,7 +414,7 @@ def main():
                              f"({args.nbatches * R * (cfg['n'] + cfg['draft'] - 1) * 4 / 1e6:.0f} MB)"},
             "us_per_row": round(elapsed / (R * args.steps) * 1e6, 5),
             "speedup_vs_radix": round(rad_t / gvr_t, 3),
-            "radix_rows_per_s": round(R * world * args.steps / rad_t, 1),
+            "radix_rows_per_s": round(rows_all * args.steps / rad_t, 1),
             "hbm_gbs": round(step_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -377,6 +429,7 @@ def main():
                                "cand_mean": float(st[:, 2].mean())},
             "gpu_launches": args.steps * (2 if args.impl == "gvr" else 1),
             "clocks": clk.summary(),
+            "allgather": gather_info,
             "check": check,
         }
     # end-to-end through the host-buffer C ABI (H2D + kernel + D2H in the timed region)
