@@ -40,9 +40,11 @@ sys.path.insert(0, ROOT)
 
 K = 2048
 CONFIGS = {
-    "cfg1": dict(requests=1, layers=1, n=8192, draft=1, desc="single decode row N=8192"),
+    "cfg1": dict(requests=1, layers=1, first_layer=30, n=8192, draft=1,
+                 desc="single decode row N=8192 (layer 30, rho ~ 0.9)"),
     "cfg2": dict(requests=8, layers=61, n=100_000, draft=1, desc="batch 8 x 61 layers, N=100K"),
-    "cfg3": dict(requests=1, layers=1, n=131_072, draft=1, desc="batch-1 long context"),
+    "cfg3": dict(requests=1, layers=1, first_layer=30, n=131_072, draft=1,
+                 desc="batch-1 long context N=131072 (layer 30, rho ~ 0.9); scripts/latency_sweep.py sweeps N"),
     "cfg4": dict(requests=16, layers=61, n=100_000, draft=4, desc="MTP-3: 16 requests x 4 tokens x 61 layers"),
     "cfg5": dict(requests=64, layers=61, n=131_072, draft=1, split=True,
                  desc="64 requests x 61 layers, N=128K, rows split across the GPUs"),
@@ -54,7 +56,7 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 
 
 # ----------------------------------------------------------------------------- inputs
-def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0):
+def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0, first_layer=0):
     """Synthetic decode batch: rows (request, layer, draft j) of length n + j from the
     Eq. 1 indexer (synth.IndexerLayer), plus prev_topk = the exact Top-K of the
     request's previous step (n - 1 keys), shared by its draft rows.
@@ -77,10 +79,11 @@ def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0):
     prev_rows = torch.zeros((nreq * layers, S), dtype=torch.float32, device=dev)
     row = 0
     for qi, q in enumerate(req_ids):
-        for l in range(layers):
+        for li in range(layers):
+            l = first_layer + li
             s = synth.splitmix64(seed, rank, q, l)
             lay = synth.IndexerLayer(S, synth.layer_rho(l, seed), s, dev)
-            prev_rows[qi * layers + l, :n - 1] = lay.scores(n - 1)
+            prev_rows[qi * layers + li, :n - 1] = lay.scores(n - 1)
             lay.step()
             for j in range(draft):
                 scores[row, :n + j] = lay.scores(n + j)
@@ -177,14 +180,40 @@ class ClockSampler:
 KERNEL_EVENT_EVERY = 4  # per-kernel events on every 4th timed step (each record costs ~2-3 us)
 
 
-def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=False):
+def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=False, flush=None):
     """Device time of `steps` calls (seconds).  With kernel_events, every
     KERNEL_EVENT_EVERY-th call is fn(batch, evs), which also records per-kernel events on
-    the launch stream; the mean per-kernel times (seconds per launch) are returned too."""
+    the launch stream; the mean per-kernel times (seconds per launch) are returned too.
+    With `flush` (a device buffer larger than L2) every call is preceded by an untimed
+    write of that buffer and timed alone with its own events (inputs smaller than L2)."""
     import torch
     for i in range(warmup):
         fn(batches[i % len(batches)])
     torch.cuda.synchronize()
+    if flush is not None:
+        total, kern, nk = 0.0, {"gvr_guess_kernel": 0.0, "gvr_topk_kernel": 0.0}, 0
+        for i in range(steps):
+            flush.fill_(float(i))  # write-only flush (the contract's "write a buffer larger than L2")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            kev = ([torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                   if kernel_events and i % KERNEL_EVENT_EVERY == 0 else None)
+            e0.record(stream)
+            if kev is not None:
+                fn(batches[i % len(batches)], kev)
+            else:
+                fn(batches[i % len(batches)])
+            e1.record(stream)
+            if sampler is not None and i == steps // 2:
+                sampler.sample_now()
+            torch.cuda.synchronize()
+            total += e0.elapsed_time(e1) / 1e3
+            if kev is not None:
+                kern["gvr_guess_kernel"] += kev[0].elapsed_time(kev[1]) / 1e3
+                kern["gvr_topk_kernel"] += kev[1].elapsed_time(kev[2]) / 1e3
+                nk += 1
+        if not kernel_events:
+            return total
+        return total, {k: v / max(nk, 1) for k, v in kern.items()} | {"sampled_steps": nk}
     sampled = [i for i in range(steps) if i % KERNEL_EVENT_EVERY == 0] if kernel_events else []
     evs = {i: [torch.cuda.Event(enable_timing=True) for _ in range(3)] for i in sampled}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -266,7 +295,8 @@ def main():
     else:
         reqs, seed_rank = cfg["requests"], rank
     batches = [make_decode_batch(reqs, cfg["layers"], cfg["n"], dev,
-                                 seed=synth.splitmix64(synth.BASE_SEED, b), draft=cfg["draft"], rank=seed_rank)
+                                 seed=synth.splitmix64(synth.BASE_SEED, b), draft=cfg["draft"], rank=seed_rank,
+                                 first_layer=cfg.get("first_layer", 0))
                for b in range(args.nbatches)]
     torch.cuda.synchronize()
     R = batches[0]["R"]
@@ -309,12 +339,24 @@ def main():
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     phys = vis.split(",")[local_rank] if vis else str(local_rank)
     kern_times = None
+    batch_bytes = sum(int(b["scores"].numel()) * 4 for b in batches)
+    flush = None
+    if batch_bytes < 2 * 126 * 2**20:  # rotated inputs fit in L2: flush before every call
+        flush = torch.zeros(256 * 2**20 // 4, dtype=torch.float32, device=dev)
+    info = gvr.kernel_info()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fused = R <= info["gvr"]["ctas_per_sm"] * sms  # one wave: the library's single-kernel path
     with ClockSampler(phys) as clk:
-        if args.impl == "gvr":
+        if args.impl == "gvr" and fused:
+            # the call is one kernel (gvr_topk_kernel, Phase 1 inside): its call events time it
+            elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk, flush=flush)
+            kern_times = {"gvr_guess_kernel": 0.0, "gvr_topk_kernel": elapsed / args.steps,
+                          "sampled_steps": args.steps}
+        elif args.impl == "gvr":
             elapsed, kern_times = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk,
-                                             kernel_events=True)
+                                             kernel_events=True, flush=flush)
         else:
-            elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk)
+            elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk, flush=flush)
     if dist is not None:
         t = torch.tensor([elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -330,7 +372,7 @@ def main():
     value = rows_total / elapsed
 
     # the other kernel, same protocol (speedup vs own radix select)
-    other_elapsed = time_steps(other_fn, batches, args.steps, args.warmup, stream)
+    other_elapsed = time_steps(other_fn, batches, args.steps, args.warmup, stream, flush=flush)
     if dist is not None:
         t = torch.tensor([other_elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -379,7 +421,7 @@ def main():
         step_gbs = abytes / (elapsed / args.steps) / 1e9  # whole call (all kernels + gaps)
         if args.impl == "gvr":
             # dominant kernel: the streaming / refine kernel, timed by its own events
-            kbytes = stream_kernel_bytes(lens_np)
+            kbytes = stream_kernel_bytes(lens_np) if not fused else abytes
             kern_s = kern_times["gvr_topk_kernel"]
         else:
             kbytes = abytes  # the radix kernel is the whole call
@@ -410,8 +452,10 @@ def main():
             "impl": args.impl,
             "config": {"workload": f"{args.config}: {cfg['desc']}", "rows_per_gpu": R, "N": cfg["n"], "K": K,
                        "draft_tokens": cfg["draft"], "parallelism": f"row-shard x{world}",
-                       "l2": f"inputs larger than L2: {args.nbatches} distinct batches rotated "
-                             f"({args.nbatches * R * (cfg['n'] + cfg['draft'] - 1) * 4 / 1e6:.0f} MB)"},
+                       "l2": (f"inputs larger than L2: {args.nbatches} distinct batches rotated "
+                              f"({batch_bytes / 1e6:.0f} MB)") if flush is None else
+                             (f"inputs ({batch_bytes / 1e6:.2f} MB) fit in L2: a 256 MB buffer is written before "
+                              f"every call (untimed), each call timed alone with CUDA events")},
             "us_per_row": round(elapsed / (R * args.steps) * 1e6, 5),
             "speedup_vs_radix": round(rad_t / gvr_t, 3),
             "radix_rows_per_s": round(rows_all * args.steps / rad_t, 1),
@@ -427,7 +471,9 @@ def main():
             "passes_per_row": {"global_mean": float(st[:, 4].mean()), "secant_mean": float(st[:, 0].mean()),
                                "snap_mean": float(st[:, 1].mean()), "raises_mean": float(st[:, 5].mean()),
                                "cand_mean": float(st[:, 2].mean())},
-            "gpu_launches": args.steps * (2 if args.impl == "gvr" else 1),
+            "gpu_launches": args.steps * (2 if args.impl == "gvr" and not fused else 1),
+            "gvr_path": ("fused single kernel (one wave)" if fused else "guess kernel + streaming kernel")
+                        if args.impl == "gvr" else None,
             "clocks": clk.summary(),
             "allgather": gather_info,
             "check": check,

@@ -521,6 +521,75 @@ __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work
 }
 
 
+// Phase 1 (Eq. 4) for one row by group c: gathers the guessed values,
+// reduces pmin / pmax / pmean and the second moment, and returns T_c, T0 (R22, R7).
+template <class G>
+__device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm)
+{
+    constexpr int GPT = KMAX / G::N;  // 8 guesses per thread
+    float gv[GPT];
+    uint32_t valid = 0;
+    if (pr) {
+        int32_t gi[GPT];
+#pragma unroll
+        for (int j = 0; j < GPT; ++j) {
+            const int q = c.tid + j * G::N;
+            gi[j] = q < k ? __ldg(pr + q) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < GPT; ++j) {
+            gv[j] = 0.f;
+            if (gi[j] >= 0 && gi[j] < p.n) {
+                gv[j] = __ldg(p.x + gi[j]);
+                valid |= 1u << j;
+            }
+        }
+    }
+    uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
+    float sum = 0.f, sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < GPT; ++j) {
+        if ((valid >> j) & 1u) {
+            const uint32_t kv = f2key(gv[j]);
+            kmn = min(kmn, kv);
+            kmx = max(kmx, kv);
+            ++cnt;
+            sum += gv[j];
+            sq += gv[j] * gv[j];
+        }
+    }
+    group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+    if (cnt == 0) {
+        // no valid guess: deterministic stride sample of M values (SPEC.md:287)
+        kmn = 0xffffffffu;
+        kmx = 0u;
+        sum = sq = 0.f;
+        const int M = min(KMAX, p.n);
+        for (int j = c.tid; j < M; j += G::N) {
+            const int q = (int)(((int64_t)j * p.n) / M);
+            const float v = __ldg(p.x + q);
+            const uint32_t kv = f2key(v);
+            kmn = min(kmn, kv);
+            kmx = max(kmx, kv);
+            ++cnt;
+            sum += v;
+            sq += v * v;
+        }
+        group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+    }
+    group_fsum2(c, sum, sq);
+    const float pmean = sum / (float)cnt;
+    const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
+    const float tcf = pmean - prm.collect_sigma * sqrtf(var);
+    GuessOut g;
+    g.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
+    if (p.n <= GVR_CAP) g.Tc = 0u;  // the whole row fits in B
+    g.T0 = f2key(pmean);
+    g.t0_ok = isfinite(pmean) ? 1 : 0;
+    g.pad = 0;
+    return g;
+}
+
 // ---------------- Phase 1: guess statistics (Eq. 4)
 // x at the previous step's Top-K positions -> pmin / pmax / pmean plus the second
 // moment; T_c = pmean - sigma * sd (R5), T0 = pmean for Phase 2.  Runs as its
@@ -555,68 +624,8 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     }
     // one strided row sample per thread, gathered alongside the guess values
     const float xs = __ldg(p.x + (int)(((int64_t)c.tid * p.n) / GUESS_NT));
-    constexpr int GPT = KMAX / GUESS_NT;  // 8 guesses per thread
     const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
-    float gv[GPT];
-    uint32_t valid = 0;
-    if (pr) {
-        int32_t gi[GPT];
-#pragma unroll
-        for (int j = 0; j < GPT; ++j) {
-            const int q = c.tid + j * GUESS_NT;
-            gi[j] = q < k ? __ldg(pr + q) : -1;
-        }
-#pragma unroll
-        for (int j = 0; j < GPT; ++j) {
-            gv[j] = 0.f;
-            if (gi[j] >= 0 && gi[j] < p.n) {
-                gv[j] = __ldg(p.x + gi[j]);
-                valid |= 1u << j;
-            }
-        }
-    }
-    uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
-    float sum = 0.f, sq = 0.f;
-#pragma unroll
-    for (int j = 0; j < GPT; ++j) {
-        if ((valid >> j) & 1u) {
-            const uint32_t kv = f2key(gv[j]);
-            kmn = min(kmn, kv);
-            kmx = max(kmx, kv);
-            ++cnt;
-            sum += gv[j];
-            sq += gv[j] * gv[j];
-        }
-    }
-    group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
-    if (cnt == 0) {
-        // no valid guess: deterministic stride sample of M values (SPEC.md:287)
-        kmn = 0xffffffffu;
-        kmx = 0u;
-        sum = sq = 0.f;
-        const int M = min(KMAX, p.n);
-        for (int j = c.tid; j < M; j += GUESS_NT) {
-            const int q = (int)(((int64_t)j * p.n) / M);
-            const float v = __ldg(p.x + q);
-            const uint32_t kv = f2key(v);
-            kmn = min(kmn, kv);
-            kmx = max(kmx, kv);
-            ++cnt;
-            sum += v;
-            sq += v * v;
-        }
-        group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
-    }
-    group_fsum2(c, sum, sq);
-    const float pmean = sum / (float)cnt;
-    const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
-    const float tcf = pmean - prm.collect_sigma * sqrtf(var);
-    GuessOut g;
-    g.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
-    if (p.n <= GVR_CAP) g.Tc = 0u;  // the whole row fits in B
-    g.T0 = f2key(pmean);
-    g.t0_ok = isfinite(pmean) ? 1 : 0;
-    g.pad = 0;
+    const GuessOut g = phase1_guess(c, p, pr, k, prm);
     const uint32_t hits = group_red1<R_ADD>(c, f2key(xs) >= g.Tc ? 1u : 0u);
     if (c.tid == 0) {
         gp[r] = g;
@@ -631,10 +640,13 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
 __global__ void __launch_bounds__(GVR_NT, 2)
 gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                 int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
-                const int32_t* __restrict__ order, long long* phase_ts)
+                const int32_t* __restrict__ order, const int32_t* prev, long long* phase_ts)
 {
+    // Split mode (gp != nullptr): Phase 1 ran in gvr_guess_kernel and CTA b processes row
+    // order[b].  Fused mode (gp == nullptr, batches of at most one wave): CTA b
+    // processes row b and runs Phase 1 itself while its first tiles load.
     extern __shared__ __align__(128) unsigned char smem[];
-    const int r = __ldg(order + blockIdx.x);
+    const int r = gp ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
     const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
                     policy_evict_first()};
     const Buf B{reinterpret_cast<uint32_t*>(smem + G_OFF_B), reinterpret_cast<int32_t*>(smem + G_OFF_B + GVR_CAP * 4),
@@ -663,8 +675,8 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         done_kind = GVR_DONE_TRIVIAL;
         st[2] = p.n;
     } else {
-        // ---------------- Phase 1 ran in gvr_guess_kernel
-        const GuessOut gq = gp[r];
+        // ---------------- Phase 1: in gvr_guess_kernel (split) or here (fused)
+        const GuessOut gq = gp ? gp[r] : phase1_guess(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm);
         RowMeta m;
         m.Tc = gq.Tc;
         m.T0 = gq.T0;

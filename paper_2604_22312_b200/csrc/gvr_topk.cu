@@ -97,6 +97,32 @@ cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lea
     return cudaSuccess;
 }
 
+// Largest batch handled by the single-launch fused path: one wave of the streaming
+// kernel (resident CTAs per SM x SMs), where the guess kernel's row ordering cannot help
+// and its extra launch and hand-off only add latency.
+int fused_max_rows()
+{
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    if (!cached[dev]) {
+        int sms = 0, per_sm = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            cudaFuncSetAttribute(gvr_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GVR_SMEM_BYTES) !=
+                cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gvr_topk_kernel, GVR_NT, GVR_SMEM_BYTES) !=
+                cudaSuccess) {
+            (void)cudaGetLastError();
+            return 0;
+        }
+        cached[dev] = sms * per_sm > 0 ? sms * per_sm : -1;
+    }
+    return cached[dev] > 0 ? cached[dev] : 0;
+}
+
 template <class Kern>
 gvr_status set_smem(Kern kern, int bytes)
 {
@@ -175,6 +201,19 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
     }
     if ((st = set_smem(gvr_topk_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;
+    auto mark = [&](int i) {
+        if (ev && ev[i]) (void)cudaEventRecord(ev[i], stream);
+    };
+    if (num_rows <= fused_max_rows()) {
+        // one wave: a single launch, Phase 1 inside each row's CTA (no hand-off, no
+        // scratch); the gathers overlap the CTA's first tile loads
+        mark(0);
+        mark(1);
+        gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
+                                                                      stats, prm, nullptr, nullptr, prev_topk, phase_ts);
+        mark(2);
+        return launch_status();
+    }
     // Phase 1 for every row (one small CTA per row), then the streaming / refine kernel
     // (one CTA per row, two CTAs per SM).  The per-row hand-off lives in the stream's
     // cached scratch (acquire_scratch), so concurrent calls on different streams do not
@@ -196,15 +235,12 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         if (lease.temporary) (void)cudaFreeAsync(scratch, stream);
         return GVR_ERR_CUDA;
     }
-    auto mark = [&](int i) {
-        if (ev && ev[i]) (void)cudaEventRecord(ev[i], stream);
-    };
     mark(0);
     gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm, gp,
                                                         sched);
     mark(1);
     gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
-                                                                  stats, prm, gp, sched.order, phase_ts);
+                                                                  stats, prm, gp, sched.order, nullptr, phase_ts);
     mark(2);
     const gvr_status ls = launch_status();
     if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
