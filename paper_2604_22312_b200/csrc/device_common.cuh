@@ -341,6 +341,36 @@ __device__ __forceinline__ int compact_ge(G& c, const Buf& B, int fill, uint32_t
     return out_base;
 }
 
+// Append the entries of B[0, fill) with key >= T to another buffer (dkey / didx, e.g. a
+// cluster peer's shared memory) at base, base+1, ..., using the cached per-chunk counts
+// of the last count pass at T.  Order-free.
+template <class G>
+__device__ __forceinline__ void push_ge(G& c, const Buf& B, int fill, uint32_t T, const ChunkCounts& cc, uint32_t* dkey,
+                                        int32_t* didx, int base)
+{
+    constexpr int CHUNK = G::N * CHUNK_SLOTS;
+    int out_base = base;
+#pragma unroll
+    for (int ch = 0; ch < NCHUNK_MAX; ++ch) {
+        if (ch * CHUNK >= fill) break;  // group-uniform
+        uint32_t tot;
+        int pos = out_base + (int)group_excl_scan(c, cc.c[ch], tot);
+#pragma unroll
+        for (int j = 0; j < CHUNK_SLOTS; ++j) {
+            const int p = ch * CHUNK + j * G::N + c.tid;
+            if (p < fill) {
+                const uint32_t kk = B.key[p];
+                if (kk >= T) {
+                    dkey[pos] = kk;
+                    didx[pos] = B.idx[p];
+                    ++pos;
+                }
+            }
+        }
+        out_base += (int)tot;
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // K-th bin search: find bin b with
 //   sum(hist[b+1..nb)) < krem <= sum(hist[b..nb)).

@@ -29,6 +29,8 @@
 //     overshooting guess (f(T_c) < K) -> exact radix select + ordered tie fill from
 //     global memory.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "pipeline.cuh"
 #include "select_global.cuh"
 
@@ -253,7 +255,7 @@ __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const R
         const uint32_t ex = group_excl_scan(c, pass, tot);
         if (pass) {
             B.key[ex] = kv;
-            B.idx[ex] = i;
+            B.idx[ex] = p.idx0 + i;
             kmax = max(kmax, kv);
         }
         if (c.tid == 0) {
@@ -275,7 +277,7 @@ __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const R
         mbar_wait(ring.full(s0), par);
         if (t0 + 1 < p.ntiles) mbar_wait(ring.full(s0 + 1), par);
         const float* sp = ring.stage(s0);
-        const int ibase = p.head + t0 * STAGE_FLOATS + lb;
+        const int ibase = p.idx0 + p.head + t0 * STAGE_FLOATS + lb;
         bool failed_here = false;
         uint32_t mask = 0;
         if (rc == 0) {
@@ -721,6 +723,265 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             s.buffer_count = ftc_stat;
             s.cluster = 1;
             stats[r] = s;
+        }
+        if (phase_ts) {
+            tsr[TS_END] = clock64();
+            tsr[TS_GEND] = global_ns();
+            tsr[TS_SMID] = sm_id();
+            for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = tsr[i];
+        }
+    }
+}
+
+// =====================================================================================
+// Cluster of G CTAs per row (BASELINE.json "one CTA or cluster per row chosen
+// by N"): for few, long rows one CTA streams too slowly (≈ 20 GB/s), so the row is cut
+// into G slices (slice_plan), each streamed by one CTA of a thread-block cluster into its
+// own buffer B_g with the common collect threshold T_c (Phase 1 is evaluated by every
+// CTA, identically).  A CTA that overflows raises its own threshold, keeping >= K of its
+// slice, so T_m = max_g T_c,g still satisfies f(T_m) >= K and, by Lemma 1, every element
+// >= T_m of the row sits in some B_g.  The CTAs then exchange (T_c,g, kmax_g) through the
+// leader's shared memory (DSMEM), count their entries >= T_m, and — after a cluster-wide
+// radix search for a higher threshold if the union would not fit — push them into the
+// leader's B (st.shared::cluster).  The leader finishes Phases 2-4 and the ordered output.
+namespace cg = cooperative_groups;
+
+constexpr int CX_OFF = 60 * 1024;  // cluster exchange area inside the (idle) ring
+enum { CX_TC = 0, CX_KMAX = 1, CX_RC = 2, CX_N = 3, CX_STRIDE = 4, CX_DEC = 32 };
+static_assert(CX_OFF + (CX_DEC + 8) * 4 <= NSTAGE * STAGE_BYTES, "exchange area fits in the ring");
+
+// Cluster-wide threshold search: every CTA histograms its own B over [base, base+width)
+// (256 bins), the leader sums the G histograms through DSMEM, picks a bin edge whose
+// count over the whole cluster lies in [K, cap] (nearest f_target) or narrows into the
+// crossing bin, and publishes the decision in its exchange area.  Returns the new
+// threshold, or 0xffffffff... flagged through ok = false when none exists (massive ties).
+__device__ __noinline__ uint32_t cluster_threshold(GvrGroup& c, const Buf& B, int fill, int32_t* hist, int32_t* lcx,
+                                                   uint32_t Tm, uint32_t kmx, int K, bool& ok)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    const int G = (int)cl.num_blocks();
+    const bool leader = cl.block_rank() == 0;
+    const uint32_t cap = (uint32_t)B.cap;
+    const uint32_t target = min((uint32_t)((K + CWIN) / 2), cap);
+    uint32_t base = Tm, above = 0;
+    uint64_t width = (uint64_t)kmx - Tm + 1ull;
+    ok = false;
+    uint32_t T = Tm;
+    for (int level = 0; level < 5; ++level) {
+        const int s = width > (uint64_t)RAISE_BINS ? 64 - __clzll((long long)(width - 1)) - 8 : 0;
+        hist[c.tid] = 0;
+        c.sync();
+        for (int p = c.tid; p < fill; p += GVR_NT) {
+            const uint32_t kk = B.key[p];
+            if (kk >= base && (uint64_t)(kk - base) < width) atomicAdd(&hist[(kk - base) >> s], 1);
+        }
+        cl.sync();  // every CTA's histogram complete and visible
+        if (leader) {
+            const int b = RAISE_BINS - 1 - c.tid;
+            uint32_t h = 0;
+            for (int q = 0; q < G; ++q) h += (uint32_t)cl.map_shared_rank(hist, q)[b];
+            uint32_t tot;
+            const uint32_t Sb = above + group_excl_scan(c, h, tot) + h;
+            uint32_t m_t = Sb >= target ? 1u : 0u, m_k = Sb >= (uint32_t)K ? 1u : 0u;
+            group_red2<R_ADD, R_ADD>(c, m_t, m_k);
+            const int bt = (int)m_t - 1, bk = (int)m_k - 1;
+            if (b == bt) c.misc[20] = (int)Sb;
+            if (b == bk) c.misc[21] = (int)Sb;
+            if (b == bk + 1) c.misc[22] = (int)Sb;
+            c.sync();
+            if (c.tid == 0) {
+                const uint32_t St = bt >= 0 ? (uint32_t)c.misc[20] : 0u;
+                const uint32_t Sk = (uint32_t)c.misc[21];
+                const uint32_t Snext = bk + 1 < RAISE_BINS ? (uint32_t)c.misc[22] : above;
+                int dec = 0;  // 0 narrow, 1 done, 2 fail
+                uint32_t Tn = 0;
+                if (bk < 0) {
+                    dec = 2;
+                } else if (bt >= 0 && St <= cap) {
+                    dec = 1;
+                    Tn = base + ((uint32_t)bt << s);
+                } else if (Sk <= cap) {
+                    dec = 1;
+                    Tn = base + ((uint32_t)bk << s);
+                } else if (s == 0) {
+                    dec = 2;
+                } else {
+                    Tn = base + ((uint32_t)bk << s);  // new base
+                }
+                lcx[CX_DEC + 0] = dec;
+                lcx[CX_DEC + 1] = (int32_t)Tn;
+                lcx[CX_DEC + 2] = s;
+                lcx[CX_DEC + 3] = (int32_t)Snext;
+            }
+        }
+        cl.sync();  // decision published
+        const int dec = lcx[CX_DEC + 0];
+        const uint32_t Tn = (uint32_t)lcx[CX_DEC + 1];
+        const int sw = lcx[CX_DEC + 2];
+        const uint32_t Snext = (uint32_t)lcx[CX_DEC + 3];
+        cl.sync();  // everyone read it before the next level overwrites the histograms
+        if (dec == 1) {
+            ok = true;
+            T = Tn;
+            break;
+        }
+        if (dec == 2) break;
+        base = Tn;
+        width = 1ull << sw;
+        above = Snext;
+    }
+    return T;
+}
+
+__global__ void __launch_bounds__(GVR_NT, 2)
+gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
+                        int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const int32_t* prev,
+                        long long* phase_ts)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int G = (int)cl.num_blocks();
+    const int g = (int)cl.block_rank();
+    const int r = (int)blockIdx.x / G;
+    const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
+                    policy_evict_first()};
+    const Buf B{reinterpret_cast<uint32_t*>(smem + G_OFF_B), reinterpret_cast<int32_t*>(smem + G_OFF_B + GVR_CAP * 4),
+                GVR_CAP};
+    const Work Wk{reinterpret_cast<int32_t*>(smem + G_OFF_WORK), reinterpret_cast<int32_t*>(smem + G_OFF_WORK + NBINS * 4),
+                  reinterpret_cast<unsigned long long*>(smem + G_OFF_WORK + 2 * NBINS * 4), GVR_CSORT};
+    int32_t* rhist = reinterpret_cast<int32_t*>(smem + G_OFF_RHIST);
+    int32_t* cx = reinterpret_cast<int32_t*>(smem + G_OFF_RING + CX_OFF);
+    GvrGroup c;
+    c.init(threadIdx.x, smem + G_OFF_SCR);
+    const int K = k;
+    const RowPlan pw = plan_row(scores, stride, row_lens, r, k);
+    const RowPlan p = slice_plan(pw, g, G);
+    const long long ts0 = phase_ts ? clock64() : 0ll;
+    if (c.tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(ring.full(s), 1);
+        fence_mbar_init();
+        for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);
+    }
+    const RowGeom geo = make_geom(pw.x, pw.n);
+    int32_t* o = out + (int64_t)r * k;
+    float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
+    int st[4] = {0, 0, 0, 0};
+    int done_kind = GVR_DONE_CONVERGED, passes = 1, raises = 0, ftc_stat = 0;
+    long long tsr[TS_N] = {ts0, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
+    if (pw.n <= k) {  // cluster-uniform: the leader emits the whole row
+        if (g != 0) return;
+        c.sync();
+        small_row_emit(c, B, Wk, geo, k, o, ov);
+        done_kind = GVR_DONE_TRIVIAL;
+        st[2] = pw.n;
+    } else {
+        // ---------------- Phase 1 (every CTA, identical result) and the slice stream
+        const GuessOut gq = phase1_guess(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm);
+        if (phase_ts) tsr[TS_PHASE1] = clock64();
+        uint32_t Tc = gq.Tc, kmax = 0u, extras = 0u;
+        int fill = 0;
+        const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras);
+        group_red2<R_MAX, R_ADD>(c, kmax, extras);
+        // ---------------- merge across the cluster (DSMEM)
+        cl.sync();  // every slice streamed; rings idle
+        int32_t* lcx = cl.map_shared_rank(cx, 0);
+        if (c.tid == 0) {
+            lcx[g * CX_STRIDE + CX_TC] = (int32_t)Tc;
+            lcx[g * CX_STRIDE + CX_KMAX] = (int32_t)kmax;
+            lcx[g * CX_STRIDE + CX_RC] = rc | (raises << 1);
+        }
+        cl.sync();
+        uint32_t Tm = 0u, kmx = 0u;
+        int any_rc = 0, raises_all = 0;
+        for (int q = 0; q < G; ++q) {
+            Tm = max(Tm, (uint32_t)lcx[q * CX_STRIDE + CX_TC]);
+            kmx = max(kmx, (uint32_t)lcx[q * CX_STRIDE + CX_KMAX]);
+            any_rc |= lcx[q * CX_STRIDE + CX_RC] & 1;
+            raises_all += lcx[q * CX_STRIDE + CX_RC] >> 1;
+        }
+        bool ok = any_rc == 0;
+        uint32_t T = Tm, tot = 0, pre = 0;
+        ChunkCounts cc;
+        if (ok) {
+            cc = count_chunks_ge(c, B, fill, T);
+            uint32_t ng = group_red1<R_ADD>(c, chunk_total(cc));
+            cl.sync();  // the exchange slots are read before they are rewritten
+            if (c.tid == 0) lcx[g * CX_STRIDE + CX_N] = (int32_t)ng;
+            cl.sync();
+            for (int q = 0; q < G; ++q) {
+                const uint32_t nq = (uint32_t)lcx[q * CX_STRIDE + CX_N];
+                tot += nq;
+                if (q < g) pre += nq;
+            }
+            if (tot > (uint32_t)B.cap) {
+                // the union does not fit the leader's buffer: raise the threshold cluster-wide
+                T = cluster_threshold(c, B, fill, rhist, lcx, Tm, kmx, K, ok);
+                if (ok) {
+                    ++raises_all;
+                    cc = count_chunks_ge(c, B, fill, T);
+                    ng = group_red1<R_ADD>(c, chunk_total(cc));
+                    if (c.tid == 0) lcx[g * CX_STRIDE + CX_N] = (int32_t)ng;
+                    cl.sync();
+                    tot = pre = 0;
+                    for (int q = 0; q < G; ++q) {
+                        const uint32_t nq = (uint32_t)lcx[q * CX_STRIDE + CX_N];
+                        tot += nq;
+                        if (q < g) pre += nq;
+                    }
+                }
+            }
+            ok = ok && tot >= (uint32_t)K;
+        }
+        if (ok) {
+            // the leader compacts its own entries in place, then the others append theirs
+            if (g == 0) fill = compact_ge(c, B, fill, T, cc);
+            cl.sync();
+            if (g != 0) {
+                uint32_t* dkey = cl.map_shared_rank(B.key, 0);
+                int32_t* didx = cl.map_shared_rank(B.idx, 0);
+                push_ge(c, B, fill, T, cc, dkey, didx, (int)pre);
+            }
+            cl.sync();  // every push has landed in the leader's buffer
+            if (g != 0) return;
+            if (phase_ts) tsr[TS_STREAM] = clock64();
+            RowMeta m;
+            m.fill = (int)tot;
+            m.Tc = T;
+            m.ftc = tot;
+            m.kmax = kmx;
+            m.extras = 0u;  // the merge compared exact keys
+            m.T0 = gq.T0;
+            m.t0_ok = gq.t0_ok != 0;
+            ftc_stat = (int)tot;
+            refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
+            if (st[3]) {
+                done_kind = GVR_DONE_TIEFILL;
+                ++passes;
+                tiefill_emit(c, B, Wk, geo, (uint32_t)c.misc[10], (uint32_t)c.misc[11], K, k, o, ov);
+            }
+        } else {
+            // massive ties or f(T_m) < K: the leader selects from global memory
+            cl.sync();
+            if (g != 0) return;
+            const RadixResult rr = radix_select_global(c, Wk, geo, (uint32_t)K, false);
+            passes += rr.rounds + 1;
+            done_kind = GVR_DONE_TIEFILL;
+            tiefill_emit(c, B, Wk, geo, rr.prefix, rr.above, K, k, o, ov);
+        }
+        raises = raises_all;
+    }
+    if (c.tid == 0) {
+        if (stats) {
+            gvr_row_stats sr;
+            sr.secant_iters = st[0];
+            sr.snap_iters = st[1];
+            sr.cand_count = st[2];
+            sr.done_kind = done_kind;
+            sr.global_passes = passes;
+            sr.raises = raises;
+            sr.buffer_count = ftc_stat;
+            sr.cluster = G;
+            stats[r] = sr;
         }
         if (phase_ts) {
             tsr[TS_END] = clock64();

@@ -204,7 +204,45 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     auto mark = [&](int i) {
         if (ev && ev[i]) (void)cudaEventRecord(ev[i], stream);
     };
-    if (num_rows <= fused_max_rows()) {
+    // Cluster geometry: G CTAs per row when the batch is small and the
+    // rows long — G = the largest power of two <= 8 with >= 16K elements per slice and
+    // num_rows * G within one wave; gvr_options.force_cluster (1, 2, 4, 8) overrides.
+    int G = 1;
+    const int wave = fused_max_rows();
+    if (opt && opt->force_cluster > 0) {
+        G = opt->force_cluster;
+        if (G != 1 && G != 2 && G != 4 && G != 8) return GVR_ERR_UNSUPPORTED;
+    } else {
+        while (G < 8 && row_stride / (2 * G) >= 16384 && (int64_t)num_rows * 2 * G <= wave) G *= 2;
+    }
+    if (G > 1) {
+        if ((st = set_smem(gvr_topk_cluster_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;
+        if ((int64_t)num_rows * G > 0x7fffffffLL) return GVR_ERR_UNSUPPORTED;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(num_rows * G));
+        cfg.blockDim = dim3(GVR_NT);
+        cfg.dynamicSmemBytes = GVR_SMEM_BYTES;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        mark(0);
+        mark(1);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, gvr_topk_cluster_kernel, scores, row_stride, row_lens, (int)k,
+                                                 out_idx, out_val, stats, prm, prev_topk, phase_ts);
+        mark(2);
+        if (e != cudaSuccess) {
+            g_last_cuda_error = e;
+            (void)cudaGetLastError();
+            return GVR_ERR_CUDA;
+        }
+        return launch_status();
+    }
+    if (num_rows <= wave) {
         // one wave: a single launch, Phase 1 inside each row's CTA (no hand-off, no
         // scratch); the gathers overlap the CTA's first tile loads
         mark(0);

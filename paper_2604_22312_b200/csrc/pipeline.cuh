@@ -65,6 +65,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 // the <= 3 scalars before it and after it are handled separately.
 struct RowPlan {
     const float* x;
+    int idx0;  // row index of x[0] (0 for a whole row, the slice start for a cluster slice)
     int n;
     int head;    // scalar elements [0, head) before the first 16-byte boundary
     int nfl;     // body floats (multiple of 4), starting at x + head (16-byte aligned)
@@ -77,6 +78,7 @@ __device__ __forceinline__ RowPlan plan_row(const float* scores, int64_t stride,
     int n = (int)stride;
     if (row_lens) n = min(max(__ldg(row_lens + r), 0), (int)stride);
     p.x = scores + (int64_t)r * stride;
+    p.idx0 = 0;
     p.n = n;
     const uintptr_t a = reinterpret_cast<uintptr_t>(p.x);
     int head = (int)(((16u - (uint32_t)(a & 15u)) & 15u) >> 2);
@@ -84,6 +86,26 @@ __device__ __forceinline__ RowPlan plan_row(const float* scores, int64_t stride,
     p.head = head;
     p.nfl = 4 * ((n - head) >> 2);
     p.ntiles = n <= k ? 0 : (p.nfl + STAGE_FLOATS - 1) / STAGE_FLOATS;
+    return p;
+}
+
+// Slice g of G of a row plan (cluster mode): the body is cut at multiples of 4 floats;
+// slice 0 keeps the unaligned head scalars, slice G-1 the tail scalars.  Every slice of
+// a streamed row is non-empty when the body holds at least 4*G floats.
+__device__ __forceinline__ RowPlan slice_plan(const RowPlan& w, int g, int G)
+{
+    const int v = w.nfl >> 2;  // body float4s
+    const int b0 = w.head + 4 * (int)(((int64_t)v * g) / G);
+    const int b1 = w.head + 4 * (int)(((int64_t)v * (g + 1)) / G);
+    RowPlan p;
+    const int start = g == 0 ? 0 : b0;
+    const int end = g == G - 1 ? w.n : b1;
+    p.x = w.x + start;
+    p.idx0 = start;
+    p.n = end - start;
+    p.head = g == 0 ? w.head : 0;
+    p.nfl = b1 - b0;
+    p.ntiles = w.ntiles == 0 ? 0 : (p.nfl + STAGE_FLOATS - 1) / STAGE_FLOATS;
     return p;
 }
 

@@ -289,3 +289,73 @@ def test_events_entry_point(gvr):
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
     assert evs[0].elapsed_time(evs[1]) > 0 and evs[1].elapsed_time(evs[2]) > 0
+
+
+# ------------------------------------------------------------------ cluster per row
+def _run_cluster(gvr, host, lens, prev, G):
+    import torch
+    dev = torch.device("cuda:0")
+    p = None if prev is None else torch.from_numpy(np.ascontiguousarray(prev, np.int32)).to(dev)
+    idx, val, st = gvr.topk_ex(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev), prev=p,
+                               options=gvr.GvrOptions(float("nan"), 0, G, 0))
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), st.cpu().numpy()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("n", [2047, 6000, 20_001, 100_000, 262_144])
+def test_cluster_rows(gvr, G, n):
+    """A cluster of G CTAs per row (slices merged into the leader through DSMEM) gives
+    the oracle's output, for good (rho 0.9) and poor (rho 0) previous-step guesses."""
+    rows, prevs = [], []
+    for i, rho in enumerate((0.9, 0.0, 0.92)):
+        p, c = synth.decode_pair(n, rho, seed=500 + 7 * i + n % 97)
+        rows.append(c.numpy())
+        prevs.append(oracle.topk(p.numpy(), K))
+    host, lens = _pack(rows)
+    got, st = _run_cluster(gvr, host, lens, np.stack(prevs), G)
+    assert np.array_equal(got, oracle.topk_batched(host, K, row_lens=lens)), st.tolist()
+    assert all(int(s[7]) == G for s in st)
+
+
+@pytest.mark.parametrize("G", [2, 8])
+@pytest.mark.parametrize("gk", ["random", "adversarial", "none", "all_minus1"])
+def test_cluster_guess_kinds(gvr, G, gk):
+    n = 120_000
+    p, c = synth.decode_pair(n, 0.9, seed=610)
+    row = c.numpy()
+    host, lens = _pack([row])
+    g = synth.guess(gk, row, K, 611)
+    got, st = _run_cluster(gvr, host, lens, None if g is None else g[None, :], G)
+    assert np.array_equal(got, oracle.topk_batched(host, K, row_lens=lens)), st.tolist()
+
+
+@pytest.mark.parametrize("kind", ["ties90", "few_distinct", "signed_zero_mix", "with_inf", "normal"])
+def test_cluster_distributions(gvr, kind):
+    rows = [synth.dist_row(kind, n, seed=620 + i) for i, n in enumerate([70_000, 33_000, 131_072])]
+    host, lens = _pack(rows)
+    prev = np.stack([synth.guess("random", r, K, 9) for r in rows])
+    for G in (4, 8):
+        got, st = _run_cluster(gvr, host, lens, prev, G)
+        assert np.array_equal(got, oracle.topk_batched(host, K, row_lens=lens)), (G, st.tolist())
+
+
+def test_cluster_ragged_and_trivial_rows(gvr):
+    rows = [synth.dist_row("normal", n, seed=630 + i) for i, n in enumerate([0, 5, 2048, 2049, 40_000, 99_999])]
+    host, lens = _pack(rows, stride=100_003)
+    got, st = _run_cluster(gvr, host, lens, None, 8)
+    assert np.array_equal(got, oracle.topk_batched(host, K, row_lens=lens)), st.tolist()
+
+
+def test_cluster_chosen_automatically_at_batch_1(gvr):
+    import torch
+    n = 131_072
+    p, c = synth.decode_pair(n, 0.9, seed=640)
+    host, lens = _pack([c.numpy()])
+    prev = oracle.topk(p.numpy(), K)[None, :]
+    dev = torch.device("cuda:0")
+    idx, _, st = gvr.topk_ex(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
+                             prev=torch.from_numpy(prev).to(dev))
+    torch.cuda.synchronize()
+    assert np.array_equal(idx.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
+    assert int(st.cpu().numpy()[0, 7]) == 8
