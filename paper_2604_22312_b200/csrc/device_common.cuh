@@ -504,9 +504,15 @@ __device__ __forceinline__ void emit_sorted(G& c, const Buf& B, const Work& Wk, 
     const uint32_t scale = bin_scale((uint64_t)kmx - Tsel + 1ull);
     bool counting = n_sel <= Wk.csort_cap;
     if (counting) {
-        for (int p = c.tid; p < fill; p += G::N) {
-            const uint32_t kv = B.key[p];
-            if (kv >= Tsel) atomicAdd(&hist[(NBINS - 1) - lin_bin(kv - Tsel, scale)], 1);
+        // loads run ahead of the (aliasing) shared atomics: UNR entries per thread per step
+        constexpr int UNR = 4;
+        for (int p0 = c.tid; p0 < fill; p0 += UNR * G::N) {
+            uint32_t kv[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) kv[u] = p0 + u * G::N < fill ? B.key[p0 + u * G::N] : 0u;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+                if (p0 + u * G::N < fill && kv[u] >= Tsel) atomicAdd(&hist[(NBINS - 1) - lin_bin(kv[u] - Tsel, scale)], 1);
         }
         c.sync();
         constexpr int BPT = NBINS / G::N;  // consecutive bins per thread
@@ -530,12 +536,22 @@ __device__ __forceinline__ void emit_sorted(G& c, const Buf& B, const Work& Wk, 
             }
             c.sync();
             unsigned long long* cs = Wk.csort;
-            for (int p = c.tid; p < fill; p += G::N) {
-                const uint32_t kv = B.key[p];
-                if (kv >= Tsel) {
-                    const int b = (NBINS - 1) - lin_bin(kv - Tsel, scale);
-                    const int slot = atomicAdd(&cur[b], 1);
-                    cs[slot] = make_comp(kv, B.idx[p]);
+            for (int p0 = c.tid; p0 < fill; p0 += UNR * G::N) {
+                uint32_t kv[UNR];
+                int32_t ix[UNR];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const int p = p0 + u * G::N;
+                    kv[u] = p < fill ? B.key[p] : 0u;
+                    ix[u] = p < fill ? B.idx[p] : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    if (p0 + u * G::N < fill && kv[u] >= Tsel) {
+                        const int b = (NBINS - 1) - lin_bin(kv[u] - Tsel, scale);
+                        const int slot = atomicAdd(&cur[b], 1);
+                        cs[slot] = make_comp(kv[u], ix[u]);
+                    }
                 }
             }
             c.sync();
@@ -549,6 +565,7 @@ __device__ __forceinline__ void emit_sorted(G& c, const Buf& B, const Work& Wk, 
                 const int cnt = hist[b];
                 const int st = cur[b] - cnt;
                 int rank = 0;
+#pragma unroll 4
                 for (int i = st; i < st + cnt; ++i) rank += cs[i] > v;
                 const int pos = st + rank;
                 if (pos < take) {
@@ -598,6 +615,123 @@ __device__ __forceinline__ void emit_sorted(G& c, const Buf& B, const Work& Wk, 
         if (out_val) out_val[j] = val;
     }
     c.sync();
+}
+
+// Phase 4 fused with the ordered output (R28): the candidates B[0, fill) (all
+// keys in [Tlo, kmx]) are counting-sorted into NBINS linear bins (bin 0 = highest keys),
+// the bin holding sorted position take-1 is found from the bin scan — the paper's K-th
+// bin search over the 2048-bin histogram — and only the bins up to it
+// are scattered and ranked (entries ranked inside their bin by the 64-bit composite, so
+// the K-th key T* is read off the sorted order instead of being snapped to).  The first
+// `take` entries are written, then -1 padding up to k.  Returns false without writing
+// when the prefix up to the K-th bin exceeds the sort capacity or one of its bins holds
+// more than CSORT_BIN_MAX entries (massive ties); the caller then runs the snap-based
+// Phase 4 and emit_sorted.  On success *tstar_out = T*.
+template <class G>
+__device__ __forceinline__ bool select_sorted(G& c, const Buf& B, const Work& Wk, int fill, uint32_t Tlo, uint32_t kmx,
+                                              int take, int k, int32_t* out, float* out_val, uint32_t* tstar_out)
+{
+    int32_t* hist = Wk.hist;
+    int32_t* cur = Wk.aux;
+    zero_ints(c, hist, NBINS);
+    c.sync();
+    const uint32_t scale = bin_scale((uint64_t)kmx - Tlo + 1ull);
+    constexpr int UNR = 4;
+    for (int p0 = c.tid; p0 < fill; p0 += UNR * G::N) {
+        uint32_t kv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) kv[u] = p0 + u * G::N < fill ? B.key[p0 + u * G::N] : 0u;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (p0 + u * G::N < fill) atomicAdd(&hist[(NBINS - 1) - lin_bin(kv[u] - Tlo, scale)], 1);
+    }
+    c.sync();
+    constexpr int BPT = NBINS / G::N;
+    const int b0 = c.tid * BPT;
+    int h[BPT];
+    uint32_t loc = 0;
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+        h[i] = hist[b0 + i];
+        loc += (uint32_t)h[i];
+    }
+    uint32_t tot;
+    const uint32_t off0 = group_excl_scan(c, loc, tot);
+    // the bin bk that holds sorted position take-1, and the end of the prefix up to it
+    {
+        uint32_t off = off0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            if ((uint32_t)(take - 1) >= off && (uint32_t)(take - 1) < off + (uint32_t)h[i]) {
+                c.misc[12] = b0 + i;
+                c.misc[13] = (int)(off + (uint32_t)h[i]);
+            }
+            off += (uint32_t)h[i];
+        }
+    }
+    c.sync();
+    const int bk = c.misc[12];
+    const int nsel = c.misc[13];
+    uint32_t mx = 0;
+#pragma unroll
+    for (int i = 0; i < BPT; ++i)
+        if (b0 + i <= bk) mx = max(mx, (uint32_t)h[i]);
+    mx = group_red1<R_MAX>(c, mx);
+    if (nsel > Wk.csort_cap || mx > (uint32_t)CSORT_BIN_MAX) return false;  // group-uniform
+    {
+        uint32_t off = off0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            cur[b0 + i] = (int)off;  // bin start; becomes the bin end after the scatter
+            off += (uint32_t)h[i];
+        }
+    }
+    c.sync();
+    unsigned long long* cs = Wk.csort;
+    for (int p0 = c.tid; p0 < fill; p0 += UNR * G::N) {
+        uint32_t kv[UNR];
+        int32_t ix[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int p = p0 + u * G::N;
+            kv[u] = p < fill ? B.key[p] : 0u;
+            ix[u] = p < fill ? B.idx[p] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (p0 + u * G::N < fill) {
+                const int b = (NBINS - 1) - lin_bin(kv[u] - Tlo, scale);
+                if (b <= bk) cs[atomicAdd(&cur[b], 1)] = make_comp(kv[u], ix[u]);
+            }
+        }
+    }
+    c.sync();
+    int32_t* fidx = B.idx;  // B is free now
+    float* fval = reinterpret_cast<float*>(B.key);
+    for (int j = c.tid; j < nsel; j += G::N) {
+        const unsigned long long v = cs[j];
+        const int b = (NBINS - 1) - lin_bin(comp_key(v) - Tlo, scale);
+        const int cnt = hist[b];
+        const int st = cur[b] - cnt;
+        int rank = 0;
+#pragma unroll 4
+        for (int i = st; i < st + cnt; ++i) rank += cs[i] > v;
+        const int pos = st + rank;
+        if (pos < take) {
+            fidx[pos] = comp_idx(v);
+            fval[pos] = key2f(comp_key(v));
+            if (pos == take - 1) c.misc[14] = (int)comp_key(v);
+        }
+    }
+    c.sync();
+    *tstar_out = (uint32_t)c.misc[14];
+    for (int j = c.tid; j < k; j += G::N) {
+        const bool in = j < take;
+        out[j] = in ? fidx[j] : -1;
+        if (out_val) out_val[j] = in ? fval[j] : 0.f;
+    }
+    c.sync();  // B is reused by the caller
+    return true;
 }
 
 }  // namespace gvr

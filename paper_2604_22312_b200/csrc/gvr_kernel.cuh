@@ -416,7 +416,20 @@ __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work
     }
     st[2] = cand;
     if (ts) ts[TS_PHASE23] = clock64();
-    // ---------------- Phase 4: exact refinement
+    // ---------------- Phase 4 fused with the ordered output (R28): histogram over the
+    // candidates, K-th bin from its scan, the bins up to it sorted -> T* and the result
+    if (cand > K) {
+        uint32_t ts_sorted = 0;
+        if (select_sorted(c, B, Wk, cand, T, kmax, K, k, o, ov, &ts_sorted)) {
+            if (ts) {
+                ts[TS_PHASE4] = clock64();
+            }
+            st[3] = 0;
+            return;
+        }
+    }
+    // ---------------- Phase 4: exact refinement — the snap-based path,
+    // taken when the K-th bin is crowded (ties) or the prefix exceeds the sort capacity
     // every candidate key lies in [T, kmax] (kmax tracked while collecting)
     uint32_t Tstar = T, nge = (uint32_t)cand;
     if (cand != K) {
@@ -430,9 +443,14 @@ __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work
             zero_ints(c, hist, NBINS);
             if (c.tid == 0) c.misc[4] = 0;
             c.sync();
-            for (int p = c.tid; p < cand; p += GVR_NT) {
-                const uint32_t kk = B.key[p];
-                if (kk >= base && (uint64_t)(kk - base) < width) atomicAdd(&hist[(kk - base) >> s], 1);
+            for (int p0 = c.tid; p0 < cand; p0 += 4 * GVR_NT) {
+                uint32_t kk[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) kk[u] = p0 + u * GVR_NT < cand ? B.key[p0 + u * GVR_NT] : 0u;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (p0 + u * GVR_NT < cand && kk[u] >= base && (uint64_t)(kk[u] - base) < width)
+                        atomicAdd(&hist[(kk[u] - base) >> s], 1);
             }
             c.sync();
             int b;
@@ -449,9 +467,14 @@ __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work
             }
             const uint64_t bw = 1ull << s;
             if (hb <= (uint32_t)LIST_MAX) {
-                for (int p = c.tid; p < cand; p += GVR_NT) {
-                    const uint32_t kk = B.key[p];
-                    if (kk >= lo_b && (uint64_t)(kk - lo_b) < bw) list[atomicAdd(&c.misc[4], 1)] = kk;
+                for (int p0 = c.tid; p0 < cand; p0 += 4 * GVR_NT) {
+                    uint32_t kk[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) kk[u] = p0 + u * GVR_NT < cand ? B.key[p0 + u * GVR_NT] : 0u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (p0 + u * GVR_NT < cand && kk[u] >= lo_b && (uint64_t)(kk[u] - lo_b) < bw)
+                            list[atomicAdd(&c.misc[4], 1)] = kk[u];
                 }
                 c.sync();
                 if (c.warp == 0) {

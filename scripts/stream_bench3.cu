@@ -193,22 +193,12 @@ int main(int argc, char** argv)
 #define RUN(NT, NS, SF, R, CAP, MODE, CPS)                                                                      \
     run(#NT "thr " #NS "x" #SF " R" #R " cap" #CAP " m" #MODE, collect<NT, NS, SF, R, CAP, MODE>, NT,          \
         NS * SF * 4 + CAP * 8 + NS * 8 + 64, CPS)
-    RUN(512, 3, 8192, 1, 8192, 0, 1);   // 0: previous best geometry, new loop
-    RUN(512, 4, 8192, 2, 8192, 0, 1);   // 1
-    RUN(512, 4, 8192, 2, 8192, 1, 1);   // 2
-    RUN(256, 4, 4096, 2, 8192, 0, 1);   // 3
-    RUN(256, 6, 4096, 2, 8192, 0, 1);   // 4
-    RUN(256, 4, 4096, 2, 4096, 0, 2);   // 5
-    RUN(256, 4, 2048, 2, 4096, 0, 2);   // 6
-    RUN(512, 4, 4096, 2, 4096, 0, 2);   // 7
-    RUN(512, 2, 8192, 2, 4096, 0, 2);   // 8
-    RUN(256, 4, 2048, 2, 4096, 0, 3);   // 9
-    RUN(256, 2, 4096, 2, 4096, 0, 3);   // 10
-    RUN(512, 4, 4096, 2, 8192, 0, 1);   // 11
-    RUN(1024, 4, 8192, 2, 8192, 0, 1);  // 12
-    RUN(1024, 2, 16384, 2, 8192, 0, 1); // 13
-    RUN(512, 6, 8192, 2, 4096, 0, 1);   // 14
-    RUN(256, 2, 4096, 2, 4096, 1, 3);   // 15
-    RUN(128, 4, 1024, 2, 4096, 0, 3);   // 16
+    // ring depth at 2 CTAs/SM (the GVR kernel's geometry); CAP shrunk to fit
+    RUN(256, 4, 4096, 2, 4096, 0, 2);   // 0: current ring (64 KB)
+    RUN(256, 6, 4096, 2, 2048, 0, 2);   // 1: 96 KB
+    RUN(256, 8, 2048, 2, 4096, 0, 2);   // 2: 64 KB in 8 x 8 KB
+    RUN(256, 6, 2048, 2, 4096, 0, 2);   // 3: 48 KB
+    RUN(256, 5, 4096, 1, 4096, 0, 2);   // 4: 80 KB, rounds of one stage
+    RUN(256, 4, 4096, 1, 4096, 0, 2);   // 5: 64 KB, rounds of one stage
     return 0;
 }
