@@ -713,9 +713,21 @@ __device__ __forceinline__ bool select_sorted(G& c, const Buf& B, const Work& Wk
         const int b = (NBINS - 1) - lin_bin(comp_key(v) - Tlo, scale);
         const int cnt = hist[b];
         const int st = cur[b] - cnt;
+        // rank inside the bin; the warp's largest bin picks a fully unrolled, predicated
+        // variant so the loads issue back to back instead of one dependent trip at a time
+        const int wmax = (int)__reduce_max_sync(__activemask(), (uint32_t)cnt);
         int rank = 0;
-#pragma unroll 4
-        for (int i = st; i < st + cnt; ++i) rank += cs[i] > v;
+        if (wmax <= 4) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (t < cnt) rank += cs[st + t] > v;
+        } else if (wmax <= 8) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (t < cnt) rank += cs[st + t] > v;
+        } else {
+            for (int i2 = st; i2 < st + cnt; ++i2) rank += cs[i2] > v;
+        }
         const int pos = st + rank;
         if (pos < take) {
             fidx[pos] = comp_idx(v);

@@ -631,7 +631,7 @@ using GuessGroup = Group<GUESS_NT, 1>;
 // the expensive rows start in the first wave instead of setting the makespan.
 struct RowSched {
     int32_t* order;    // [num_rows]: CTA b of the streaming kernel processes row order[b]
-    int32_t* cursors;  // [2]: front / back fill counts, zeroed before the launch
+    int32_t* cursors;  // [3]: front / back fill counts, finished streaming CTAs (zero at launch)
 };
 
 __global__ void __launch_bounds__(GUESS_NT)
@@ -665,7 +665,7 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
 __global__ void __launch_bounds__(GVR_NT, 2)
 gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                 int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
-                const int32_t* __restrict__ order, const int32_t* prev, long long* phase_ts)
+                const int32_t* __restrict__ order, const int32_t* prev, long long* phase_ts, int32_t* ctl)
 {
     // Split mode (gp != nullptr): Phase 1 ran in gvr_guess_kernel and CTA b processes row
     // order[b].  Fused mode (gp == nullptr, batches of at most one wave): CTA b
@@ -752,6 +752,12 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             tsr[TS_GEND] = global_ns();
             tsr[TS_SMID] = sm_id();
             for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = tsr[i];
+        }
+        // split mode: the last CTA to finish resets the scheduling cursors for the next call
+        if (ctl && atomicAdd(ctl + 2, 1) == (int)gridDim.x - 1) {
+            ctl[0] = 0;
+            ctl[1] = 0;
+            ctl[2] = 0;
         }
     }
 }

@@ -65,6 +65,7 @@ cudaMemPool_t scratch_pool()
 struct ScratchLease {
     unsigned char* ptr = nullptr;
     bool temporary = false;  // free after the launch (capture-time allocation)
+    bool fresh = false;      // newly allocated: its control words must be zeroed
 };
 
 cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lease)
@@ -86,6 +87,7 @@ cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lea
     }
     if (cap != cudaStreamCaptureStatusNone) {
         lease.temporary = true;
+        lease.fresh = true;
         return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&lease.ptr), bytes, pool, stream);
     }
     const size_t grow = bytes > 2 * slot.second ? bytes : 2 * slot.second;
@@ -94,6 +96,7 @@ cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lea
     if (slot.first) (void)cudaFreeAsync(slot.first, stream);  // stream-ordered after earlier users
     slot = std::make_pair(p, grow);
     lease.ptr = static_cast<unsigned char*>(p);
+    lease.fresh = true;
     return cudaSuccess;
 }
 
@@ -248,7 +251,8 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         mark(0);
         mark(1);
         gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
-                                                                      stats, prm, nullptr, nullptr, prev_topk, phase_ts);
+                                                                      stats, prm, nullptr, nullptr, prev_topk, phase_ts,
+                                                                      nullptr);
         mark(2);
         return launch_status();
     }
@@ -256,19 +260,21 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     // (one CTA per row, two CTAs per SM).  The per-row hand-off lives in the stream's
     // cached scratch (acquire_scratch), so concurrent calls on different streams do not
     // share it and steady-state calls allocate nothing.
-    // scratch: GuessOut[num_rows] | order[num_rows] | cursors[2]
+    // scratch: ctl[4] | GuessOut[num_rows] | order[num_rows].  ctl = {front cursor, back
+    // cursor, finished CTAs, 0} lives at a fixed offset and is zero between calls: the
+    // streaming kernel's last CTA resets it, so only a new buffer needs a memset.
     const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
-    const size_t scratch_bytes = gp_bytes + (size_t)num_rows * 4 + 8;
+    const size_t scratch_bytes = 16 + gp_bytes + (size_t)num_rows * 4;
     ScratchLease lease;
     if (acquire_scratch(stream, scratch_bytes, lease) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
     unsigned char* scratch = lease.ptr;
-    GuessOut* gp = reinterpret_cast<GuessOut*>(scratch);
-    RowSched sched{reinterpret_cast<int32_t*>(scratch + gp_bytes),
-                   reinterpret_cast<int32_t*>(scratch + gp_bytes + (size_t)num_rows * 4)};
-    if (cudaMemsetAsync(sched.cursors, 0, 8, stream) != cudaSuccess) {
+    int32_t* ctl = reinterpret_cast<int32_t*>(scratch);
+    GuessOut* gp = reinterpret_cast<GuessOut*>(scratch + 16);
+    RowSched sched{reinterpret_cast<int32_t*>(scratch + 16 + gp_bytes), ctl};
+    if (lease.fresh && cudaMemsetAsync(ctl, 0, 16, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         if (lease.temporary) (void)cudaFreeAsync(scratch, stream);
         return GVR_ERR_CUDA;
@@ -278,7 +284,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
                                                         sched);
     mark(1);
     gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
-                                                                  stats, prm, gp, sched.order, nullptr, phase_ts);
+                                                                  stats, prm, gp, sched.order, nullptr, phase_ts, ctl);
     mark(2);
     const gvr_status ls = launch_status();
     if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
