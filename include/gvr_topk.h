@@ -79,7 +79,7 @@ typedef struct {
 
 /* Tuning knobs; NULL selects the defaults.  None of them changes the result. */
 typedef struct {
-    float collect_sigma;      /* T_c = pmean - collect_sigma * sd(guess values); default 0.5 */
+    float collect_sigma;      /* T_c = pmean - collect_sigma * sd(guess values); default 0.3 */
     int32_t max_secant_iters; /* secant steps before pure bisection; default 8              */
     int32_t force_cluster;    /* 0 = automatic; else CTAs per row (1,2,4,8)                */
     int32_t reserved;

@@ -197,7 +197,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     if (prev_topk && prev_topk != out_idx && ranges_overlap(prev_topk, bytes, out_idx, bytes))
         return GVR_ERR_INVALID_ARGUMENT;
     GvrParams prm;
-    prm.collect_sigma = 0.5f;
+    prm.collect_sigma = 0.3f;  // DESIGN.md R22: measured sweep (cfg2, cfg4)
     prm.max_secant = 8;
     if (opt) {
         if (opt->collect_sigma == opt->collect_sigma) prm.collect_sigma = opt->collect_sigma;
