@@ -82,7 +82,9 @@ typedef struct {
     float collect_sigma;      /* T_c = pmean - collect_sigma * sd(guess values); default 0.3 */
     int32_t max_secant_iters; /* secant steps before pure bisection; default 8              */
     int32_t force_cluster;    /* 0 = automatic; else CTAs per row (1,2,4,8)                */
-    int32_t reserved;
+    int32_t guess_stride;     /* Phase-1 statistics over every n-th guessed position;      */
+                              /* 0 = default 4 (R29); 1 = all of them, as in    */
+                              /* PAPER.md:449-457.  Never changes the result.             */
 } gvr_options;
 
 /* GVR exact Top-K.  prev_topk: nullable device int32 [num_rows, k], the previous

@@ -34,7 +34,7 @@ MAX_K = 2048
 
 class GvrOptions(ctypes.Structure):
     _fields_ = [("collect_sigma", ctypes.c_float), ("max_secant_iters", ctypes.c_int32),
-                ("force_cluster", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("force_cluster", ctypes.c_int32), ("guess_stride", ctypes.c_int32)]
 
 
 class GvrError(RuntimeError):

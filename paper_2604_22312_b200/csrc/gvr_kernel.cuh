@@ -39,6 +39,7 @@ namespace gvr {
 struct GvrParams {
     float collect_sigma;
     int max_secant;
+    int guess_stride;  // Phase-1 statistics over every guess_stride-th guessed position (R29)
 };
 
 constexpr int GVR_NT = 256;
@@ -85,7 +86,8 @@ struct GuessOut {
     uint32_t Tc;    // collect threshold key
     uint32_t T0;    // f2key(pmean), the Phase-2 start
     int32_t t0_ok;  // pmean finite
-    int32_t pad;
+    uint32_t tmin;  // second-pass threshold: pmin when all k guesses were gathered and
+                    // valid (then f(pmin) >= k for distinct guesses), else 0 (everything)
 };
 
 // What the streaming pass hands to Phases 2-4.
@@ -563,6 +565,8 @@ template <class G>
 __device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm)
 {
     constexpr int GPT = KMAX / G::N;  // 8 guesses per thread
+    // subsampled statistics only for long rows (K/N <= 1/32, R29)
+    const int stride = p.n >= 32 * k ? prm.guess_stride : 1;
     float gv[GPT];
     uint32_t valid = 0;
     if (pr) {
@@ -570,7 +574,7 @@ __device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const i
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
             const int q = c.tid + j * G::N;
-            gi[j] = q < k ? __ldg(pr + q) : -1;
+            gi[j] = (q < k && q % stride == 0) ? __ldg(pr + q) : -1;
         }
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
@@ -616,13 +620,17 @@ __device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const i
     group_fsum2(c, sum, sq);
     const float pmean = sum / (float)cnt;
     const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
-    const float tcf = pmean - prm.collect_sigma * sqrtf(var);
+    // width of the collect threshold (R22): rows with K/N > 1/8 need a wider margin
+    // (scripts/sigma_by_n.py: at N = 8192 sigma 0.3 undershoots on 88% of rows, 0.7 on none)
+    float sg = prm.collect_sigma;
+    if (sg >= 0.f && p.n < 8 * k) sg = fmaxf(sg, 0.7f);
+    const float tcf = pmean - sg * sqrtf(var);
     GuessOut g;
     g.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
     if (p.n <= GVR_CAP) g.Tc = 0u;  // the whole row fits in B
     g.T0 = f2key(pmean);
     g.t0_ok = isfinite(pmean) ? 1 : 0;
-    g.pad = 0;
+    g.tmin = (stride == 1 && cnt == (uint32_t)k && kmn < g.Tc) ? kmn : 0u;
     return g;
 }
 
@@ -727,9 +735,46 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         m.extras = extras;
         m.ftc = (uint32_t)m.fill - extras;
         if (phase_ts) tsr[TS_STREAM] = clock64();
-        if (rc || m.ftc < (uint32_t)K) {
-            // massive ties, or f(T_c) < K (the guess overshot): exact radix select +
-            // ordered tie fill from global memory (R12/R13)
+        if (rc == 0 && m.ftc < (uint32_t)K) {
+            // f(T_c) < K (the guess overshot the K-th value): stream the row once more at
+            // a threshold that cannot undershoot — pmin of a complete guess, else -inf —
+            // with the usual raises keeping >= K (R30); bounded at two HBM passes
+            c.sync();
+            if (c.tid == 0) {
+                for (int s2 = 0; s2 < NSTAGE; ++s2) {
+                    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(ring.full(s2)) : "memory");
+                    mbar_init(ring.full(s2), 1);
+                }
+                fence_mbar_init();
+                for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);
+            }
+            m.Tc = gq.tmin;
+            kmax = 0u;
+            extras = 0u;
+            const int rc2 = stream_row(c, ring, p, B, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST), m.Tc, m.fill, K,
+                                       raises, kmax, extras);
+            group_red2<R_MAX, R_ADD>(c, kmax, extras);
+            m.kmax = kmax;
+            m.extras = extras;
+            m.ftc = (uint32_t)m.fill - extras;
+            ++passes;
+            if (rc2 == 0 && m.ftc >= (uint32_t)K) {
+                ftc_stat = (int)m.ftc;
+                refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
+                if (st[3]) {
+                    done_kind = GVR_DONE_TIEFILL;
+                    ++passes;
+                    tiefill_emit(c, B, Wk, g, (uint32_t)c.misc[10], (uint32_t)c.misc[11], K, k, o, ov);
+                }
+            } else {
+                const RadixResult rr = radix_select_global(c, Wk, g, (uint32_t)K, false);
+                passes += rr.rounds + 1;
+                done_kind = GVR_DONE_TIEFILL;
+                tiefill_emit(c, B, Wk, g, rr.prefix, rr.above, K, k, o, ov);
+            }
+        } else if (rc) {
+            // massive ties: exact radix select + ordered tie fill from global memory
+            // (R12/R13)
             const RadixResult rr = radix_select_global(c, Wk, g, (uint32_t)K, false);
             passes += rr.rounds + 1;
             done_kind = GVR_DONE_TIEFILL;
@@ -918,59 +963,86 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
         // ---------------- Phase 1 (every CTA, identical result) and the slice stream
         const GuessOut gq = phase1_guess(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm);
         if (phase_ts) tsr[TS_PHASE1] = clock64();
-        uint32_t Tc = gq.Tc, kmax = 0u, extras = 0u;
-        int fill = 0;
-        const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras);
-        group_red2<R_MAX, R_ADD>(c, kmax, extras);
-        // ---------------- merge across the cluster (DSMEM)
-        cl.sync();  // every slice streamed; rings idle
-        int32_t* lcx = cl.map_shared_rank(cx, 0);
-        if (c.tid == 0) {
-            lcx[g * CX_STRIDE + CX_TC] = (int32_t)Tc;
-            lcx[g * CX_STRIDE + CX_KMAX] = (int32_t)kmax;
-            lcx[g * CX_STRIDE + CX_RC] = rc | (raises << 1);
-        }
-        cl.sync();
-        uint32_t Tm = 0u, kmx = 0u;
-        int any_rc = 0, raises_all = 0;
-        for (int q = 0; q < G; ++q) {
-            Tm = max(Tm, (uint32_t)lcx[q * CX_STRIDE + CX_TC]);
-            kmx = max(kmx, (uint32_t)lcx[q * CX_STRIDE + CX_KMAX]);
-            any_rc |= lcx[q * CX_STRIDE + CX_RC] & 1;
-            raises_all += lcx[q * CX_STRIDE + CX_RC] >> 1;
-        }
-        bool ok = any_rc == 0;
-        uint32_t T = Tm, tot = 0, pre = 0;
+        uint32_t Tc = gq.Tc, kmax = 0u, extras = 0u, Tm = 0u, kmx = 0u, T = 0u, tot = 0, pre = 0;
+        int fill = 0, raises_all = 0;
+        bool ok = false;
         ChunkCounts cc;
-        if (ok) {
-            cc = count_chunks_ge(c, B, fill, T);
-            uint32_t ng = group_red1<R_ADD>(c, chunk_total(cc));
-            cl.sync();  // the exchange slots are read before they are rewritten
-            if (c.tid == 0) lcx[g * CX_STRIDE + CX_N] = (int32_t)ng;
-            cl.sync();
-            for (int q = 0; q < G; ++q) {
-                const uint32_t nq = (uint32_t)lcx[q * CX_STRIDE + CX_N];
-                tot += nq;
-                if (q < g) pre += nq;
+        int32_t* lcx = cl.map_shared_rank(cx, 0);
+        for (int pass = 0;; ++pass) {
+            if (pass == 1) {
+                // f(T_m) < K: every slice is streamed once more at a threshold that cannot
+                // undershoot (R30)
+                c.sync();
+                if (c.tid == 0) {
+                    for (int s2 = 0; s2 < NSTAGE; ++s2) {
+                        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(ring.full(s2)) : "memory");
+                        mbar_init(ring.full(s2), 1);
+                    }
+                    fence_mbar_init();
+                    for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);
+                }
+                Tc = gq.tmin;
+                kmax = 0u;
+                extras = 0u;
+                fill = 0;
+                ++passes;
             }
-            if (tot > (uint32_t)B.cap) {
-                // the union does not fit the leader's buffer: raise the threshold cluster-wide
-                T = cluster_threshold(c, B, fill, rhist, lcx, Tm, kmx, K, ok);
-                if (ok) {
-                    ++raises_all;
-                    cc = count_chunks_ge(c, B, fill, T);
-                    ng = group_red1<R_ADD>(c, chunk_total(cc));
-                    if (c.tid == 0) lcx[g * CX_STRIDE + CX_N] = (int32_t)ng;
-                    cl.sync();
-                    tot = pre = 0;
-                    for (int q = 0; q < G; ++q) {
-                        const uint32_t nq = (uint32_t)lcx[q * CX_STRIDE + CX_N];
-                        tot += nq;
-                        if (q < g) pre += nq;
+            const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras);
+            group_red2<R_MAX, R_ADD>(c, kmax, extras);
+            // ---------------- merge across the cluster (DSMEM)
+            cl.sync();  // every slice streamed; rings idle
+            if (c.tid == 0) {
+                lcx[g * CX_STRIDE + CX_TC] = (int32_t)Tc;
+                lcx[g * CX_STRIDE + CX_KMAX] = (int32_t)kmax;
+                lcx[g * CX_STRIDE + CX_RC] = rc | (raises << 1);
+            }
+            cl.sync();
+            Tm = 0u;
+            kmx = 0u;
+            int any_rc = 0;
+            raises_all = 0;
+            for (int q = 0; q < G; ++q) {
+                Tm = max(Tm, (uint32_t)lcx[q * CX_STRIDE + CX_TC]);
+                kmx = max(kmx, (uint32_t)lcx[q * CX_STRIDE + CX_KMAX]);
+                any_rc |= lcx[q * CX_STRIDE + CX_RC] & 1;
+                raises_all += lcx[q * CX_STRIDE + CX_RC] >> 1;
+            }
+            ok = any_rc == 0;
+            T = Tm;
+            tot = pre = 0;
+            if (ok) {
+                cc = count_chunks_ge(c, B, fill, T);
+                uint32_t ng = group_red1<R_ADD>(c, chunk_total(cc));
+                cl.sync();  // the exchange slots are read before they are rewritten
+                if (c.tid == 0) lcx[g * CX_STRIDE + CX_N] = (int32_t)ng;
+                cl.sync();
+                for (int q = 0; q < G; ++q) {
+                    const uint32_t nq = (uint32_t)lcx[q * CX_STRIDE + CX_N];
+                    tot += nq;
+                    if (q < g) pre += nq;
+                }
+                if (tot > (uint32_t)B.cap) {
+                    // the union does not fit the leader's buffer: raise the threshold cluster-wide
+                    T = cluster_threshold(c, B, fill, rhist, lcx, Tm, kmx, K, ok);
+                    if (ok) {
+                        ++raises_all;
+                        cc = count_chunks_ge(c, B, fill, T);
+                        ng = group_red1<R_ADD>(c, chunk_total(cc));
+                        if (c.tid == 0) lcx[g * CX_STRIDE + CX_N] = (int32_t)ng;
+                        cl.sync();
+                        tot = pre = 0;
+                        for (int q = 0; q < G; ++q) {
+                            const uint32_t nq = (uint32_t)lcx[q * CX_STRIDE + CX_N];
+                            tot += nq;
+                            if (q < g) pre += nq;
+                        }
                     }
                 }
             }
-            ok = ok && tot >= (uint32_t)K;
+            const bool under = ok && tot < (uint32_t)K;  // cluster-uniform
+            ok = ok && !under;
+            if (!under || pass == 1) break;
+            cl.sync();  // the exchange area (inside the rings) is read before the rings refill
         }
         if (ok) {
             // the leader compacts its own entries in place, then the others append theirs

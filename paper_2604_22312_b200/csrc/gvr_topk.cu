@@ -199,7 +199,12 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     GvrParams prm;
     prm.collect_sigma = 0.3f;  // DESIGN.md R22: measured sweep (cfg2, cfg4)
     prm.max_secant = 8;
+#ifndef GVR_DEFAULT_GUESS_STRIDE
+#define GVR_DEFAULT_GUESS_STRIDE 4  // DESIGN.md R29
+#endif
+    prm.guess_stride = GVR_DEFAULT_GUESS_STRIDE;
     if (opt) {
+        if (opt->guess_stride > 0) prm.guess_stride = opt->guess_stride;
         if (opt->collect_sigma == opt->collect_sigma) prm.collect_sigma = opt->collect_sigma;
         if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
     }

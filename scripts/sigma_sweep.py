@@ -12,6 +12,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--sigmas", default="0.5,0.45,0.4,0.35,0.3,0.25")
 ap.add_argument("--steps", type=int, default=30)
+ap.add_argument("--stride", type=int, default=0, help="guess_stride option (0 = library default)")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 dev = torch.device("cuda:0")
@@ -22,7 +23,7 @@ R = batches[0]["R"]
 out = torch.empty((R, bench.K), dtype=torch.int32, device=dev)
 F = gvr.STATS_FIELDS
 for s in [float(x) for x in args.sigmas.split(",")]:
-    opt = gvr.GvrOptions(s, 0, 0, 0)
+    opt = gvr.GvrOptions(s, 0, 0, args.stride)
     stats = []
     for b in batches:
         _, _, st = gvr.topk_ex(b["scores"], bench.K, row_lens=b["row_lens"], prev=b["prev"], out=out, values=False,
@@ -45,7 +46,7 @@ for s in [float(x) for x in args.sigmas.split(",")]:
     us = e0.elapsed_time(e1) * 1e3 / args.steps
     col = lambda n: st[:, F.index(n)]
     bc = col("buffer_count")
-    print(f"sigma {s:4.2f}: {us:7.1f} us/step  raises/row {col('raises').mean():.2f} (rows>0 {np.mean(col('raises') > 0):.2f})"
+    print(f"stride {args.stride} sigma {s:4.2f}: {us:7.1f} us/step  raises/row {col('raises').mean():.2f} (rows>0 {np.mean(col('raises') > 0):.2f})"
           f"  f(Tc) p10/50/90 {np.percentile(bc, 10):.0f}/{np.percentile(bc, 50):.0f}/{np.percentile(bc, 90):.0f}"
           f"  fallback {np.mean(col('done_kind') >= 2):.3f}  secant {col('secant_iters').mean():.2f}"
           f"  snap {col('snap_iters').mean():.2f}  cand {col('cand_count').mean():.0f}", flush=True)

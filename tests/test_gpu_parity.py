@@ -359,3 +359,49 @@ def test_cluster_chosen_automatically_at_batch_1(gvr):
     torch.cuda.synchronize()
     assert np.array_equal(idx.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
     assert int(st.cpu().numpy()[0, 7]) == 8
+
+
+@pytest.mark.parametrize("gk", ["prev", "random", "adversarial"])
+def test_guess_stride_never_changes_result(gvr, gk):
+    """Phase-1 statistics over every guess_stride-th guessed position (R29) change only the
+    collect threshold, never the output: strides 1 (the paper's all positions), 2, 4."""
+    import torch
+    dev = torch.device("cuda:0")
+    rows, prevs = [], []
+    for i in range(5):
+        p, c = synth.decode_pair(90_000, 0.9 if i % 2 else 0.0, seed=700 + i)
+        rows.append(c.numpy())
+        prevs.append(synth.guess(gk, rows[-1], K, 701 + i, prev_topk=oracle.topk(p.numpy(), K)))
+    host, lens = _pack(rows)
+    ref = oracle.topk_batched(host, K, row_lens=lens)
+    s = torch.from_numpy(host).to(dev)
+    l = torch.from_numpy(lens).to(dev)
+    pv = torch.from_numpy(np.stack(prevs).astype(np.int32)).to(dev)
+    for stride in (1, 2, 4):
+        idx, _, _ = gvr.topk_ex(s, K, row_lens=l, prev=pv, options=gvr.GvrOptions(float("nan"), 0, 0, stride))
+        torch.cuda.synchronize()
+        assert np.array_equal(idx.cpu().numpy(), ref), stride
+
+
+@pytest.mark.parametrize("n", [8192, 20_000, 100_000, 262_144])
+def test_guess_overshoot_takes_a_second_pass(gvr, n):
+    """f(T_c) < K (a perfect guess, or T_c forced above pmean) -> the row is streamed once
+    more at pmin / -inf (R30): exact result, at most two HBM passes."""
+    import torch
+    dev = torch.device("cuda:0")
+    rows = [synth.dist_row(kind, n, seed=800 + i) for i, kind in enumerate(["normal", "lognormal", "uniform"])]
+    p, c = synth.decode_pair(n, 0.9, seed=810)
+    rows.append(c.numpy())
+    host, lens = _pack(rows)
+    ref = oracle.topk_batched(host, K, row_lens=lens)
+    perfect = np.stack([oracle.topk(r, K) for r in rows]).astype(np.int32)  # the current Top-K itself
+    s = torch.from_numpy(host).to(dev)
+    l = torch.from_numpy(lens).to(dev)
+    for sigma, stride in ((0.3, 1), (-1.0, 1), (-1.0, 4)):
+        idx, _, st = gvr.topk_ex(s, K, row_lens=l, prev=torch.from_numpy(perfect).to(dev),
+                                 options=gvr.GvrOptions(sigma, 0, 0, stride))
+        torch.cuda.synchronize()
+        st = st.cpu().numpy()
+        assert np.array_equal(idx.cpu().numpy(), ref), (sigma, stride, st.tolist())
+        if sigma < 0:
+            assert (st[:, 4] == 2).all() and (st[:, 3] == 1).all(), st.tolist()  # two passes, converged
