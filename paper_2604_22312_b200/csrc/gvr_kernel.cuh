@@ -144,7 +144,7 @@ __device__ __forceinline__ int rel_off(int e) { return ((e & ~3) << 5) | (e & 3)
 // no such T exists (massive ties).  mx = max key over B and the held elements.
 __device__ __noinline__ int raise_threshold(GvrGroup& c, const Buf& B, int32_t* hist, const float* sp, int lb,
                                             uint32_t held, uint32_t& Tc, int& fill, uint32_t mx, float phi, int K,
-                                            int& raises)
+                                            int& raises, uint32_t& tie_key)
 {
     const uint32_t acc_hi = (uint32_t)B.cap / 2;
     const float ft = 0.5f * (float)(K + CWIN);
@@ -198,6 +198,14 @@ __device__ __noinline__ int raise_threshold(GvrGroup& c, const Buf& B, int32_t* 
             if (Sk <= (uint32_t)B.cap && base + (uint32_t)bk != Tc) {
                 T = base + (uint32_t)bk;
                 rc = 0;
+            } else if (base + (uint32_t)bk < 0xffffffffu) {
+                // massive ties at v = base + bk (more than the buffer holds, fewer than K
+                // above it so far): keep collecting only keys > v.  If the row ends with
+                // fewer than K keys > v, v is the K-th key and the caller runs the ordered
+                // tie fill (R13); otherwise later raises continue as usual.
+                tie_key = base + (uint32_t)bk;
+                T = tie_key + 1u;
+                rc = 0;
             }
             break;
         }
@@ -239,7 +247,7 @@ __device__ __forceinline__ void write_candidates(const Buf& B, const float* sp, 
 // still waited for, so no copy is in flight when the ring is reused).
 __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const RowPlan& p, const Buf& B,
                                           int32_t* rhist, uint32_t& Tc, int& fill, int K, int& raises, uint32_t& kmax,
-                                          uint32_t& extras)
+                                          uint32_t& extras, uint32_t& tie_key)
 {
     int* fillp = c.misc + 16;     // reservation cursor
     int* failbase = c.misc + 17;  // lowest failed reservation of the round
@@ -320,7 +328,7 @@ __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const R
             uint32_t mx = kmax;
             for (uint32_t m = held; m; m &= m - 1) mx = max(mx, f2key(sp[lb + rel_off(__ffs(m) - 1)]));
             mx = group_red1<R_MAX>(c, mx);
-            const int rr = raise_threshold(c, B, rhist, sp, lb, held, Tc, f, mx, phi, K, raises);
+            const int rr = raise_threshold(c, B, rhist, sp, lb, held, Tc, f, mx, phi, K, raises, tie_key);
             if (rr) {
                 rc = 1;
             } else {
@@ -727,15 +735,21 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
         m.t0_ok = gq.t0_ok != 0;
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         // ---------------- streaming pass (HBM read once, TMA ring)
-        uint32_t kmax = 0u, extras = 0u;
+        uint32_t kmax = 0u, extras = 0u, tie_key = 0u;
         const int rc = stream_row(c, ring, p, B, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST), m.Tc, m.fill, K, raises,
-                                  kmax, extras);
+                                  kmax, extras, tie_key);
         group_red2<R_MAX, R_ADD>(c, kmax, extras);
         m.kmax = kmax;
         m.extras = extras;
         m.ftc = (uint32_t)m.fill - extras;
         if (phase_ts) tsr[TS_STREAM] = clock64();
-        if (rc == 0 && m.ftc < (uint32_t)K) {
+        if (rc == 0 && m.ftc < (uint32_t)K && tie_key != 0u) {
+            // massive ties at tie_key and fewer than K keys above it in the whole row:
+            // tie_key is the K-th key; ordered tie fill (one more pass, R13)
+            done_kind = GVR_DONE_TIEFILL;
+            ++passes;
+            tiefill_emit(c, B, Wk, g, tie_key, m.ftc, K, k, o, ov);
+        } else if (rc == 0 && m.ftc < (uint32_t)K) {
             // f(T_c) < K (the guess overshot the K-th value): stream the row once more at
             // a threshold that cannot undershoot — pmin of a complete guess, else -inf —
             // with the usual raises keeping >= K (R30); bounded at two HBM passes
@@ -751,14 +765,19 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             m.Tc = gq.tmin;
             kmax = 0u;
             extras = 0u;
+            uint32_t tie2 = 0u;
             const int rc2 = stream_row(c, ring, p, B, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST), m.Tc, m.fill, K,
-                                       raises, kmax, extras);
+                                       raises, kmax, extras, tie2);
             group_red2<R_MAX, R_ADD>(c, kmax, extras);
             m.kmax = kmax;
             m.extras = extras;
             m.ftc = (uint32_t)m.fill - extras;
             ++passes;
-            if (rc2 == 0 && m.ftc >= (uint32_t)K) {
+            if (rc2 == 0 && m.ftc < (uint32_t)K && tie2 != 0u) {
+                done_kind = GVR_DONE_TIEFILL;
+                ++passes;
+                tiefill_emit(c, B, Wk, g, tie2, m.ftc, K, k, o, ov);
+            } else if (rc2 == 0 && m.ftc >= (uint32_t)K) {
                 ftc_stat = (int)m.ftc;
                 refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
                 if (st[3]) {
@@ -987,7 +1006,8 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
                 fill = 0;
                 ++passes;
             }
-            const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras);
+            uint32_t tie_unused = 0u;  // cluster slices: ties end in the leader's fallback
+            const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras, tie_unused);
             group_red2<R_MAX, R_ADD>(c, kmax, extras);
             // ---------------- merge across the cluster (DSMEM)
             cl.sync();  // every slice streamed; rings idle
