@@ -405,3 +405,35 @@ def test_guess_overshoot_takes_a_second_pass(gvr, n):
         assert np.array_equal(idx.cpu().numpy(), ref), (sigma, stride, st.tolist())
         if sigma < 0:
             assert (st[:, 4] == 2).all() and (st[:, 3] == 1).all(), st.tolist()  # two passes, converged
+
+
+def test_split_path_ragged_trivial_and_mixed_guesses(gvr):
+    """More than one wave of rows (guess kernel + streaming kernel with row scheduling):
+    ragged lengths including empty and len <= k rows, every guess kind, value
+    distributions; exact against the oracle."""
+    import torch
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(11)
+    R = 340  # > 2 x 148 resident CTAs: the split path
+    lens = rng.integers(0, 40_000, size=R).astype(np.int32)
+    lens[:6] = [0, 1, 2047, 2048, 2049, 40_000]
+    S = int(lens.max())
+    host = np.zeros((R, S), np.float32)
+    kinds = synth.DISTRIBUTIONS
+    prev = np.full((R, K), -1, np.int32)
+    for r in range(R):
+        n = int(lens[r])
+        if n == 0:
+            continue
+        row = synth.dist_row(kinds[r % len(kinds)], n, seed=900 + r)
+        host[r, :n] = row
+        g = synth.guess(synth.GUESS_KINDS[r % 6], row, K, 901 + r, prev_topk=oracle.topk(row, K))
+        if g is not None:
+            prev[r] = g
+    ref = oracle.topk_batched(host, K, row_lens=lens)
+    out = gvr.topk(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
+                   prev=torch.from_numpy(prev).to(dev))
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    bad = np.argwhere((got != ref).any(axis=1))[:, 0]
+    assert bad.size == 0, f"{bad.size} rows differ, first {bad[:5].tolist()} lens {lens[bad[:5]].tolist()}"
