@@ -665,6 +665,8 @@ __global__ void __launch_bounds__(GUESS_NT)
 gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens,
                  const int32_t* prev, int k, int num_rows, GvrParams prm, GuessOut* __restrict__ gp, RowSched sched)
 {
+    // the streaming kernel may be scheduled now; it waits for this grid before reading
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __shared__ __align__(16) unsigned char scratch[GROUP_SCRATCH_BYTES];
     GuessGroup c;
     c.init(threadIdx.x, scratch);
@@ -698,7 +700,10 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
     // order[b].  Fused mode (gp == nullptr, batches of at most one wave): CTA b
     // processes row b and runs Phase 1 itself while its first tiles load.
     extern __shared__ __align__(128) unsigned char smem[];
-    const int r = gp ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+    // split mode runs under programmatic dependent launch: wait for the guess grid (its
+    // writes are visible after this) before reading the row order and the hand-off
+    if (gp) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int r = gp ? order[blockIdx.x] : (int)blockIdx.x;
     const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
                     policy_evict_first()};
     const Buf B{reinterpret_cast<uint32_t*>(smem + G_OFF_B), reinterpret_cast<int32_t*>(smem + G_OFF_B + GVR_CAP * 4),

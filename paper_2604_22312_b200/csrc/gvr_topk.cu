@@ -288,8 +288,29 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm, gp,
                                                         sched);
     mark(1);
-    gvr_topk_kernel<<<num_rows, GVR_NT, GVR_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
-                                                                  stats, prm, gp, sched.order, nullptr, phase_ts, ctl);
+    {
+        // programmatic dependent launch: scheduled while the guess kernel runs, the
+        // streaming kernel waits for it (griddepcontrol.wait) before reading the hand-off;
+        // serialised when per-kernel events are recorded between the two
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)num_rows);
+        cfg.blockDim = dim3(GVR_NT);
+        cfg.dynamicSmemBytes = GVR_SMEM_BYTES;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = ev ? 0 : 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, gvr_topk_kernel, scores, row_stride, row_lens, (int)k, out_idx,
+                                                 out_val, stats, prm, static_cast<const GuessOut*>(gp),
+                                                 static_cast<const int32_t*>(sched.order),
+                                                 static_cast<const int32_t*>(nullptr), phase_ts, ctl);
+        if (e != cudaSuccess) {
+            g_last_cuda_error = e;
+            (void)cudaGetLastError();
+        }
+    }
     mark(2);
     const gvr_status ls = launch_status();
     if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
