@@ -103,11 +103,13 @@ def algorithmic_bytes(lens, k=K):
     return int(4 * int(np.sum(lens)) + len(lens) * (4 * k + 4 * k + 4))
 
 
-def stream_kernel_bytes(lens, k=K):
-    """Algorithmic bytes of the streaming / refine kernel alone (gvr_topk_kernel): the
-    row read once (4N), the output written (4K) and the row length (4); the guess read
-    and its gathers belong to gvr_guess_kernel."""
-    return int(4 * int(np.sum(lens)) + len(lens) * (4 * k + 4))
+def stream_kernel_bytes(lens, k=K, path="filter"):
+    """Algorithmic bytes of the streaming kernel alone.  Filter path (gvr_filter_kernel):
+    the row read once (4N) and the row length (4); its candidate lists are intermediate.
+    Row path (gvr_topk_kernel): the row (4N), the output written (4K) and the row length.
+    The guess read and its gathers belong to gvr_guess_kernel."""
+    per_row = 4 if path == "filter" else 4 * k + 4
+    return int(4 * int(np.sum(lens)) + len(lens) * per_row)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -191,11 +193,11 @@ def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=F
         fn(batches[i % len(batches)])
     torch.cuda.synchronize()
     if flush is not None:
-        total, kern, nk = 0.0, {"gvr_guess_kernel": 0.0, "gvr_topk_kernel": 0.0}, 0
+        total, kern, nk = 0.0, {"guess": 0.0, "stream": 0.0, "refine": 0.0}, 0
         for i in range(steps):
             flush.fill_(float(i))  # write-only flush (the contract's "write a buffer larger than L2")
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            kev = ([torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            kev = ([torch.cuda.Event(enable_timing=True) for _ in range(4)]
                    if kernel_events and i % KERNEL_EVENT_EVERY == 0 else None)
             e0.record(stream)
             if kev is not None:
@@ -208,14 +210,15 @@ def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=F
             torch.cuda.synchronize()
             total += e0.elapsed_time(e1) / 1e3
             if kev is not None:
-                kern["gvr_guess_kernel"] += kev[0].elapsed_time(kev[1]) / 1e3
-                kern["gvr_topk_kernel"] += kev[1].elapsed_time(kev[2]) / 1e3
+                kern["guess"] += kev[0].elapsed_time(kev[1]) / 1e3
+                kern["stream"] += kev[1].elapsed_time(kev[2]) / 1e3
+                kern["refine"] += kev[2].elapsed_time(kev[3]) / 1e3
                 nk += 1
         if not kernel_events:
             return total
         return total, {k: v / max(nk, 1) for k, v in kern.items()} | {"sampled_steps": nk}
     sampled = [i for i in range(steps) if i % KERNEL_EVENT_EVERY == 0] if kernel_events else []
-    evs = {i: [torch.cuda.Event(enable_timing=True) for _ in range(3)] for i in sampled}
+    evs = {i: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for i in sampled}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for i in range(steps):
@@ -230,9 +233,9 @@ def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=F
     total = ev0.elapsed_time(ev1) / 1e3
     if not kernel_events:
         return total
-    guess = sum(e[0].elapsed_time(e[1]) for e in evs.values()) / 1e3 / len(evs)
-    main = sum(e[1].elapsed_time(e[2]) for e in evs.values()) / 1e3 / len(evs)
-    return total, {"gvr_guess_kernel": guess, "gvr_topk_kernel": main, "sampled_steps": len(evs)}
+    def mean(a, b):
+        return sum(e[a].elapsed_time(e[b]) for e in evs.values()) / 1e3 / len(evs)
+    return total, {"guess": mean(0, 1), "stream": mean(1, 2), "refine": mean(2, 3), "sampled_steps": len(evs)}
 
 
 def cpu_oracle_rate(host_scores, lens, max_rows=None, threads=None):
@@ -258,6 +261,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="verify every batch against the oracle")
+    ap.add_argument("--path", default="filter", choices=["filter", "row"],
+                    help="batch path of the library (gvr_options.batch_path): filter kernel + refine, or row kernel")
     ap.add_argument("--gather", action="store_true",
                     help="N > 1: also time the optional NCCL all-gather of out_idx (reported separately)")
     args = ap.parse_args()
@@ -305,11 +310,16 @@ def main():
     for b in batches:
         b["out"] = torch.empty((R, K), dtype=torch.int32, device=dev)
 
+    opts = None
+    if args.path == "row":
+        opts = gvr.GvrOptions(float("nan"), 0, 0, 0, 1)
+
     def gvr_step(b, evs=None):
         if evs is None:
-            gvr.topk(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"])
+            gvr.topk(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"], options=opts)
         else:
-            gvr.topk_events(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"], events=evs)
+            gvr.topk_events(b["scores"], K, row_lens=b["row_lens"], prev=b["prev"], out=b["out"], events=evs,
+                            options=opts)
 
     def radix_step(b):
         gvr.radix_topk(b["scores"], K, row_lens=b["row_lens"], out=b["out"])
@@ -350,7 +360,7 @@ def main():
         if args.impl == "gvr" and fused:
             # the call is one kernel (gvr_topk_kernel, Phase 1 inside): its call events time it
             elapsed = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk, flush=flush)
-            kern_times = {"gvr_guess_kernel": 0.0, "gvr_topk_kernel": elapsed / args.steps,
+            kern_times = {"guess": 0.0, "stream": elapsed / args.steps, "refine": 0.0,
                           "sampled_steps": args.steps}
         elif args.impl == "gvr":
             elapsed, kern_times = time_steps(main_fn, batches, args.steps, args.warmup, stream, sampler=clk,
@@ -418,11 +428,24 @@ def main():
         peak = float(peaks.get("hbm_gbs", 6650.0))
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
         abytes = algorithmic_bytes(lens_np)
+        if fused:
+            stream_kernel, n_kernels, gvr_path = "gvr_topk_kernel", 1, "fused single kernel (one wave)"
+        elif args.path == "filter":
+            stream_kernel, n_kernels = "gvr_filter_kernel", 3
+            gvr_path = "guess kernel + filter kernel (whole batch, one HBM pass) + refine kernel (one CTA per row)"
+        else:
+            stream_kernel, n_kernels, gvr_path = "gvr_topk_kernel", 2, "guess kernel + row streaming kernel"
+
+        def kernel_us(kt):
+            names = {"guess": "gvr_guess_kernel", "stream": stream_kernel,
+                     "refine": "gvr_topk_kernel (refine)" if stream_kernel == "gvr_filter_kernel" else None}
+            d = {names[k]: round(kt[k] * 1e6, 2) for k in ("guess", "stream", "refine") if names[k]}
+            return d | {"sampled_steps": kt["sampled_steps"]}
         step_gbs = abytes / (elapsed / args.steps) / 1e9  # whole call (all kernels + gaps)
         if args.impl == "gvr":
             # dominant kernel: the streaming / refine kernel, timed by its own events
-            kbytes = stream_kernel_bytes(lens_np) if not fused else abytes
-            kern_s = kern_times["gvr_topk_kernel"]
+            kbytes = stream_kernel_bytes(lens_np, path=args.path) if not fused else abytes
+            kern_s = kern_times["stream"]
         else:
             kbytes = abytes  # the radix kernel is the whole call
             kern_s = elapsed / args.steps
@@ -463,17 +486,15 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes,
-                         "kernel": "gvr_topk_kernel" if args.impl == "gvr" else "radix_topk_kernel",
+                         "kernel": stream_kernel if args.impl == "gvr" else "radix_topk_kernel",
                          "kernel_us_per_launch": round(kern_s * 1e6, 2),
                          "step_gbs": round(step_gbs, 1)},
-            "kernel_us_per_launch": ({k: round(kern_times[k] * 1e6, 2) for k in ("gvr_guess_kernel", "gvr_topk_kernel")}
-                                     | {"sampled_steps": kern_times["sampled_steps"]} if kern_times else None),
+            "kernel_us_per_launch": (kernel_us(kern_times) if kern_times else None),
             "passes_per_row": {"global_mean": float(st[:, 4].mean()), "secant_mean": float(st[:, 0].mean()),
                                "snap_mean": float(st[:, 1].mean()), "raises_mean": float(st[:, 5].mean()),
                                "cand_mean": float(st[:, 2].mean())},
-            "gpu_launches": args.steps * (2 if args.impl == "gvr" and not fused else 1),
-            "gvr_path": ("fused single kernel (one wave)" if fused else "guess kernel + streaming kernel")
-                        if args.impl == "gvr" else None,
+            "gpu_launches": args.steps * (n_kernels if args.impl == "gvr" else 1),
+            "gvr_path": gvr_path if args.impl == "gvr" else None,
             "clocks": clk.summary(),
             "allgather": gather_info,
             "check": check,

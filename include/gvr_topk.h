@@ -85,6 +85,10 @@ typedef struct {
     int32_t guess_stride;     /* Phase-1 statistics over every n-th guessed position;      */
                               /* 0 = default 4 (R29); 1 = all of them, as in    */
                               /* PAPER.md:449-457.  Never changes the result.             */
+    int32_t batch_path;       /* batches of more than one wave: 0 = filter path            */
+                              /* (gvr_filter_kernel streams the whole batch, then one     */
+                              /* refine CTA per row); 1 = row path (one CTA streams and   */
+                              /* refines each row).  Never changes the result.           */
 } gvr_options;
 
 /* GVR exact Top-K.  prev_topk: nullable device int32 [num_rows, k], the previous
@@ -106,16 +110,19 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
                                int32_t* out_idx, cudaStream_t stream, const gvr_options* opt,
                                float* out_val, gvr_row_stats* stats);
 
-/* Same as gvr_topk_batched, and records caller-created CUDA events (cudaEventCreate;
- * any may be NULL) on `stream` right before the Phase-1 guess kernel (guess_start),
- * between it and the streaming / refine kernel (stream_start), and after that kernel
- * (stream_end), so the caller can time each kernel of the call with
- * cudaEventElapsedTime (the benchmark's per-kernel roofline).  Ownership of the events
- * stays with the caller. */
+/* Same as gvr_topk_batched_ex (opt nullable; no values or stats), and records
+ * caller-created CUDA events (cudaEventCreate; any may be NULL) on `stream`: right before
+ * the Phase-1 guess kernel (guess_start), before the streaming kernel (stream_start),
+ * after it (stream_end) and at the end of the call (call_end).  The streaming kernel is
+ * gvr_filter_kernel on the batch filter path (then stream_end .. call_end times the
+ * refine kernel), else gvr_topk_kernel (then stream_end == call_end).  For the caller's
+ * per-kernel timing (the benchmark's roofline).  Events are not launches: recording them
+ * between the kernels serialises the programmatic dependent launches.  Ownership of the
+ * events stays with the caller. */
 gvr_status gvr_topk_batched_events(const float* scores, int64_t row_stride, const int32_t* row_lens,
                                    int32_t num_rows, const int32_t* prev_topk, int32_t k, int32_t* out_idx,
                                    cudaStream_t stream, cudaEvent_t guess_start, cudaEvent_t stream_start,
-                                   cudaEvent_t stream_end);
+                                   cudaEvent_t stream_end, cudaEvent_t call_end, const gvr_options* opt);
 
 /* Per-phase timing of the GVR kernel (the paper's GVR_PHASE_TIMING instrumentation,
  * PAPER.md:1645-1656): phase_ts is a device int64 [num_rows, 9] array receiving clock64()

@@ -34,7 +34,8 @@ MAX_K = 2048
 
 class GvrOptions(ctypes.Structure):
     _fields_ = [("collect_sigma", ctypes.c_float), ("max_secant_iters", ctypes.c_int32),
-                ("force_cluster", ctypes.c_int32), ("guess_stride", ctypes.c_int32)]
+                ("force_cluster", ctypes.c_int32), ("guess_stride", ctypes.c_int32),
+                ("batch_path", ctypes.c_int32)]
 
 
 class GvrError(RuntimeError):
@@ -58,7 +59,7 @@ def _load():
         "gvr_workspace_destroy": [vp],
         "gvr_topk_batched_host": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
         "gvr_topk_phase_timing": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
-        "gvr_topk_batched_events": [vp, i64, vp, i32, vp, i32, vp, vp, vp, vp, vp],
+        "gvr_topk_batched_events": [vp, i64, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -136,11 +137,15 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def topk(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None):
+def topk(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None, options=None):
     """GVR exact ordered Top-K of every row (launch is stream-ordered, no host sync)."""
     R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
-    _check(_load().gvr_topk_batched(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
-                                    _ptr(out), _stream_ptr(stream)))
+    if options is None:
+        _check(_load().gvr_topk_batched(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
+                                        _ptr(out), _stream_ptr(stream)))
+    else:
+        _check(_load().gvr_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k,
+                                           _ptr(out), _stream_ptr(stream), ctypes.byref(options), None, None))
     return out
 
 
@@ -160,12 +165,14 @@ def topk_ex(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, values: 
 PHASES = ("phase1", "stream", "phase2_3", "phase4", "output")
 
 
-def topk_events(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, events=(None, None, None),
-                stream=None):
-    """gvr.topk that also records three torch.cuda.Events (each may be None) before the
-    guess kernel, between the two kernels and after the streaming kernel."""
+def topk_events(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, events=(None, None, None, None),
+                stream=None, options=None):
+    """gvr.topk that also records four torch.cuda.Events (each may be None): before the
+    guess kernel, before and after the streaming kernel (gvr_filter_kernel on the batch
+    filter path, else gvr_topk_kernel) and at the end of the call."""
     R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
     hs = []
+    events = tuple(events) + (None,) * (4 - len(events))
     for e in events:
         if e is None:
             hs.append(None)
@@ -173,8 +180,9 @@ def topk_events(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, even
             if e.cuda_event == 0:  # created lazily by torch: force creation
                 e.record()
             hs.append(ctypes.c_void_p(e.cuda_event))
+    opt = ctypes.byref(options) if options is not None else None
     _check(_load().gvr_topk_batched_events(_ptr(scores), stride, _ptr(row_lens), R, _ptr(prev), k, _ptr(out),
-                                           _stream_ptr(stream), *hs))
+                                           _stream_ptr(stream), *hs, opt))
     return out
 
 

@@ -90,6 +90,55 @@ struct GuessOut {
                     // valid (then f(pmin) >= k for distinct guesses), else 0 (everything)
 };
 
+// Batch path (filter_kernel.cuh): where gvr_filter_kernel left each row's candidates.
+constexpr int F_SEGS = 4;  // most filter CTAs covering one row (host-enforced)
+// Partition of the virtual tile sequence [0, V) over G CTAs: CTA b owns [V b / G, V (b+1) / G).
+struct CandLists {
+    uint2* region;  // [G][reg]: (key, idx) entries, CTA b from region + b * reg
+    int4* rec;      // [num_rows][F_SEGS]: {cta, start, end, 0}, slot = cta - cta_of(first tile)
+    long long V;    // num_rows * tpr
+    int G;          // filter CTAs
+    int tpr;        // virtual tiles per row = ceil(row_stride / STAGE_FLOATS)
+    int reg;        // region capacity per CTA (entries); entries past it are dropped
+};
+
+__host__ __device__ __forceinline__ long long cl_begin(const CandLists& cl, int b) { return cl.V * b / cl.G; }
+// The CTA whose range holds virtual tile v: the largest b with floor(V b / G) <= v.
+__host__ __device__ __forceinline__ int cl_cta_of(const CandLists& cl, long long v)
+{
+    return (int)(((v + 1) * cl.G + cl.V - 1) / cl.V) - 1;
+}
+
+// Batch filter path hand-over between the kernels (scratch; every word is zero between
+// calls).  Rows enter the ready queue when their candidate list is complete (the filter
+// CTA finishing a row's last segment pushes it; gvr_guess_kernel pushes rows with no
+// tiles); gvr_refine_kernel pops them in that order and appends the rows it cannot
+// finish to the fixup list, which gvr_topk_kernel (fixup mode) works off last.
+enum { Q_HEAD = 0, Q_TAIL = 1, Q_NFIX = 2, Q_WORDS = 4 };
+struct BatchQueue {
+    int32_t* qctl;     // [Q_WORDS]
+    int32_t* queue;    // [num_rows]: row + 1 once pushed, reset to 0 when popped
+    int32_t* segdone;  // [num_rows]: finished filter segments, reset when popped
+    int32_t* fixlist;  // [num_rows]
+};
+
+__device__ __forceinline__ int ld_relaxed(const int32_t* p)
+{
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_acquire(const int32_t* p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // What the streaming pass hands to Phases 2-4.
 struct RowMeta {
     int fill;         // entries in B
@@ -661,9 +710,45 @@ struct RowSched {
     int32_t* cursors;  // [3]: front / back fill counts, finished streaming CTAs (zero at launch)
 };
 
+constexpr int SQ_N = 1024;  // row samples for the threshold of a poor-guess row
+
+// The rank-th largest of the SQ_N keys in sq (1 <= rank <= SQ_N): most-significant-digit
+// radix select, 8 bits per level over a 256-bin histogram (one bin per thread).
+__device__ __forceinline__ uint32_t sample_rank_key(GuessGroup& c, const uint32_t* sq, int32_t* sh, int rank)
+{
+    uint32_t prefix = 0u, pmask = 0u, rem = (uint32_t)rank;
+    c.sync();  // sq complete
+    for (int level = 0; level < 4; ++level) {
+        const int shift = 24 - 8 * level;
+        sh[c.tid] = 0;
+        c.sync();
+#pragma unroll
+        for (int j = 0; j < SQ_N / GUESS_NT; ++j) {
+            const uint32_t kk = sq[c.tid + j * GUESS_NT];
+            if ((kk & pmask) == prefix) atomicAdd(&sh[(kk >> shift) & 255u], 1);
+        }
+        c.sync();
+        const int bin = 255 - c.tid;  // thread t owns bin 255 - t: descending digit order
+        const uint32_t h = (uint32_t)sh[bin];
+        uint32_t tot;
+        const uint32_t ex = group_excl_scan(c, h, tot);
+        if (ex < rem && ex + h >= rem) {
+            c.misc[0] = bin;
+            c.misc[1] = (int)ex;
+        }
+        c.sync();
+        prefix |= (uint32_t)c.misc[0] << shift;
+        pmask |= 255u << shift;
+        rem -= (uint32_t)c.misc[1];
+        c.sync();
+    }
+    return prefix;
+}
+
 __global__ void __launch_bounds__(GUESS_NT)
 gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens,
-                 const int32_t* prev, int k, int num_rows, GvrParams prm, GuessOut* __restrict__ gp, RowSched sched)
+                 const int32_t* prev, int k, int num_rows, GvrParams prm, GuessOut* __restrict__ gp, RowSched sched,
+                 BatchQueue bq)
 {
     // the streaming kernel may be scheduled now; it waits for this grid before reading
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -672,6 +757,9 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     c.init(threadIdx.x, scratch);
     const int r = blockIdx.x;
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
+    // batch filter path: a row with no tiles never reaches the filter kernel; it goes to
+    // the ready queue now (the refine kernel hands it on to the fixup list)
+    if (bq.queue && p.ntiles == 0 && c.tid == 0) st_release(bq.queue + atomicAdd(bq.qctl + Q_TAIL, 1), r + 1);
     if (p.n <= k) {  // trivial row: no guess needed (block-uniform); scheduled last
         if (c.tid == 0) sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
         return;
@@ -679,11 +767,31 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     // one strided row sample per thread, gathered alongside the guess values
     const float xs = ld_gather(p.x + (int)(((int64_t)c.tid * p.n) / GUESS_NT));
     const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
-    const GuessOut g = phase1_guess(c, p, pr, k, prm);
+    GuessOut g = phase1_guess(c, p, pr, k, prm);
     const uint32_t hits = group_red1<R_ADD>(c, f2key(xs) >= g.Tc ? 1u : 0u);
+    const bool heavy = (double)hits * p.n > (double)GVR_CAP * GUESS_NT;  // estimated f(T_c) > capacity
+    if (heavy && p.n >= 4 * k) {
+        // poor guess (low Top-K overlap, e.g. layers 0-1): its statistics
+        // put T_c far below the K-th value.  Take the threshold from a strided sample of
+        // SQ_N row values instead: the r-th largest sample key, r chosen so that about
+        // f_s = 2.5 k + 512 elements are expected at or above it (sampling error of
+        // f(T_s)/f_s ~ 1/sqrt(r); an undershoot only costs the row a second stream).
+        __shared__ uint32_t sq[SQ_N];
+        __shared__ int32_t sh[GUESS_NT];
+#pragma unroll
+        for (int j = 0; j < SQ_N / GUESS_NT; ++j) {
+            const int q = c.tid + j * GUESS_NT;
+            sq[q] = f2key(ld_gather(p.x + (int)(((int64_t)q * p.n) / SQ_N)));
+        }
+        const int rank = (int)ceil((2.5 * k + 512.0) * SQ_N / p.n);
+        const uint32_t Ts = sample_rank_key(c, sq, sh, rank < SQ_N ? rank : SQ_N);
+        if (Ts > g.Tc) {
+            g.Tc = Ts;
+            g.tmin = 0u;
+        }
+    }
     if (c.tid == 0) {
         gp[r] = g;
-        const bool heavy = (double)hits * p.n > (double)GVR_CAP * GUESS_NT;  // estimated f(T_c) > capacity
         if (heavy)
             sched.order[atomicAdd(sched.cursors, 1)] = r;
         else
@@ -691,19 +799,28 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     }
 }
 
-__global__ void __launch_bounds__(GVR_NT, 2)
-gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
-                int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
-                const int32_t* __restrict__ order, const int32_t* prev, long long* phase_ts, int32_t* ctl)
+// Split / fixup mode: the last CTA of the grid resets the scheduling cursors and the batch
+// queue's control words for the next call.
+__device__ __forceinline__ void fixup_done(int32_t* ctl, const BatchQueue& bq, int tid)
 {
-    // Split mode (gp != nullptr): Phase 1 ran in gvr_guess_kernel and CTA b processes row
-    // order[b].  Fused mode (gp == nullptr, batches of at most one wave): CTA b
-    // processes row b and runs Phase 1 itself while its first tiles load.
+    if (tid == 0 && ctl && atomicAdd(ctl + 2, 1) == (int)gridDim.x - 1) {
+        ctl[0] = 0;
+        ctl[1] = 0;
+        ctl[2] = 0;
+        if (bq.qctl)
+            for (int i = 0; i < Q_WORDS; ++i) bq.qctl[i] = 0;
+    }
+}
+
+// One row, the whole path: Phase 1 (or its hand-off), the streaming pass, Phases 2-4 and
+// the ordered output, with every fallback.  A CTA calls it once per row (reinit: the ring
+// barriers were used by a previous row of this CTA).
+__device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64_t stride,
+                                      const int32_t* __restrict__ row_lens, int k, int32_t* out, float* out_val,
+                                      gvr_row_stats* stats, const GvrParams& prm, const GuessOut* __restrict__ gp,
+                                      const int32_t* prev, long long* phase_ts, int r, bool reinit)
+{
     extern __shared__ __align__(128) unsigned char smem[];
-    // split mode runs under programmatic dependent launch: wait for the guess grid (its
-    // writes are visible after this) before reading the row order and the hand-off
-    if (gp) asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int r = gp ? order[blockIdx.x] : (int)blockIdx.x;
     const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
                     policy_evict_first()};
     const Buf B{reinterpret_cast<uint32_t*>(smem + G_OFF_B), reinterpret_cast<int32_t*>(smem + G_OFF_B + GVR_CAP * 4),
@@ -715,8 +832,12 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
     const int K = k;
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
     const long long ts0 = phase_ts ? clock64() : 0ll;
+    if (reinit) c.sync();  // every wait on the previous row's barriers is over
     if (c.tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) mbar_init(ring.full(s), 1);
+        for (int s = 0; s < NSTAGE; ++s) {
+            if (reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(ring.full(s)) : "memory");
+            mbar_init(ring.full(s), 1);
+        }
         fence_mbar_init();
         for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);  // the first 64 KB load during Phase 1
     }
@@ -833,13 +954,41 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
             tsr[TS_SMID] = sm_id();
             for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = tsr[i];
         }
-        // split mode: the last CTA to finish resets the scheduling cursors for the next call
-        if (ctl && atomicAdd(ctl + 2, 1) == (int)gridDim.x - 1) {
-            ctl[0] = 0;
-            ctl[1] = 0;
-            ctl[2] = 0;
-        }
     }
+}
+
+__global__ void __launch_bounds__(GVR_NT, 2)
+gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
+                int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
+                const int32_t* __restrict__ order, const int32_t* prev, long long* phase_ts, int32_t* ctl)
+{
+    // Split mode (gp != nullptr): Phase 1 ran in gvr_guess_kernel and CTA b processes row
+    // order[b]; it runs under programmatic dependent launch: wait for the guess grid (its
+    // writes are visible after this) before reading the row order and the hand-off.
+    // Fused mode (gp == nullptr, batches of at most one wave): CTA b processes row b and
+    // runs Phase 1 itself while its first tiles load.
+    if (gp) asm volatile("griddepcontrol.wait;" ::: "memory");
+    topk_row(scores, stride, row_lens, k, out, out_val, stats, prm, gp, prev, phase_ts,
+             gp ? order[blockIdx.x] : (int)blockIdx.x, false);
+    fixup_done(ctl, BatchQueue{}, threadIdx.x);
+}
+
+// Batch filter path, last step: the rows gvr_refine_kernel could not finish from their
+// candidate lists (an overflowed or too short list, massive ties, rows with no tiles) are
+// streamed and refined in full — CTA b takes fixup-list entries b, b + G, ...  One CTA per
+// SM (the loop needs more registers than the row kernel's two-per-SM budget); the list is
+// usually empty.  The last CTA resets the batch queue's control words.
+__global__ void __launch_bounds__(GVR_NT, 1)
+gvr_fixup_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
+                 int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
+                 const int32_t* prev, long long* phase_ts, int32_t* ctl, BatchQueue bq)
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the refine grid's fixup list is complete
+    const int nfix = ld_relaxed(bq.qctl + Q_NFIX);
+    for (int li = (int)blockIdx.x; li < nfix; li += (int)gridDim.x)
+        topk_row(scores, stride, row_lens, k, out, out_val, stats, prm, gp, prev, phase_ts, __ldcg(bq.fixlist + li),
+                 li != (int)blockIdx.x);
+    fixup_done(ctl, bq, threadIdx.x);
 }
 
 // =====================================================================================

@@ -7,6 +7,7 @@
 
 #include "../../include/gvr_topk.h"
 #include "gvr_kernel.cuh"
+#include "refine_kernel.cuh"
 #include "radix_kernel.cuh"
 
 namespace {
@@ -57,21 +58,36 @@ cudaMemPool_t scratch_pool()
     return pools[dev];
 }
 
-// Per-(device, stream) scratch for the guess-kernel hand-off, grown stream-ordered
-// from scratch_pool() and then reused: steady-state calls allocate nothing (CUDA-Graph
-// friendly).  Calls on one stream are serialised by the stream, so one buffer per
-// stream is race-free.  While the stream is being captured the cache is not modified:
-// a too-small cache is bypassed with an allocation / free pair recorded in the graph.
+// Per-(device, stream) scratch of the batch path, grown stream-ordered from scratch_pool()
+// and then reused: steady-state calls allocate nothing (CUDA-Graph friendly).  Calls on
+// one stream are serialised by the stream, so one buffer per stream is race-free.  While
+// the stream is being captured the cache is not modified: a too-small cache is bypassed
+// with an allocation / free pair recorded in the graph.
+//
+// Layout: a zero region at fixed offsets — ctl[4] | qctl[4] | queue[rows_cap] |
+// segdone[rows_cap] — whose words are zero between calls (each kernel resets what it
+// used), sized by the lease's row capacity so that calls with fewer rows leave the tail
+// untouched; then the per-call arrays (zero_region_bytes(rows_cap) onwards).
 struct ScratchLease {
     unsigned char* ptr = nullptr;
+    int64_t rows_cap = 0;
     bool temporary = false;  // free after the launch (capture-time allocation)
-    bool fresh = false;      // newly allocated: its control words must be zeroed
+    bool fresh = false;      // newly allocated: its zero region must be cleared
 };
 
-cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lease)
+size_t zero_region_bytes(int64_t rows_cap) { return (32 + 8 * (size_t)rows_cap + 255) & ~(size_t)255; }
+
+// bytes_after(rows_cap): bytes needed past the zero region for this call
+template <class F>
+cudaError_t acquire_scratch(cudaStream_t stream, int64_t rows, F bytes_after, ScratchLease& lease)
 {
+    struct Slot {
+        void* ptr = nullptr;
+        size_t size = 0;
+        int64_t rows_cap = 0;
+    };
     static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+    static std::map<std::pair<int, cudaStream_t>, Slot> cache;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -80,22 +96,29 @@ cudaError_t acquire_scratch(cudaStream_t stream, size_t bytes, ScratchLease& lea
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if ((e = cudaStreamIsCapturing(stream, &cap)) != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
-    auto& slot = cache[std::make_pair(dev, stream)];
-    if (slot.second >= bytes) {
-        lease.ptr = static_cast<unsigned char*>(slot.first);
+    Slot& slot = cache[std::make_pair(dev, stream)];
+    if (slot.ptr && slot.rows_cap >= rows && slot.size >= zero_region_bytes(slot.rows_cap) + bytes_after(slot.rows_cap)) {
+        lease.ptr = static_cast<unsigned char*>(slot.ptr);
+        lease.rows_cap = slot.rows_cap;
         return cudaSuccess;
     }
+    const int64_t rc = rows > slot.rows_cap ? rows : slot.rows_cap;
+    const size_t need = zero_region_bytes(rc) + bytes_after(rc);
     if (cap != cudaStreamCaptureStatusNone) {
         lease.temporary = true;
         lease.fresh = true;
-        return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&lease.ptr), bytes, pool, stream);
+        lease.rows_cap = rc;
+        return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&lease.ptr), need, pool, stream);
     }
-    const size_t grow = bytes > 2 * slot.second ? bytes : 2 * slot.second;
+    const size_t grow = need > 2 * slot.size ? need : 2 * slot.size;
     void* p = nullptr;
     if ((e = cudaMallocFromPoolAsync(&p, grow, pool, stream)) != cudaSuccess) return e;
-    if (slot.first) (void)cudaFreeAsync(slot.first, stream);  // stream-ordered after earlier users
-    slot = std::make_pair(p, grow);
+    if (slot.ptr) (void)cudaFreeAsync(slot.ptr, stream);  // stream-ordered after earlier users
+    slot.ptr = p;
+    slot.size = grow;
+    slot.rows_cap = rc;
     lease.ptr = static_cast<unsigned char*>(p);
+    lease.rows_cap = rc;
     lease.fresh = true;
     return cudaSuccess;
 }
@@ -130,7 +153,12 @@ template <class Kern>
 gvr_status set_smem(Kern kern, int bytes)
 {
     // Opt in to > 48 KB dynamic shared memory; idempotent and cheap.
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    // Every kernel also prefers the largest shared-memory carveout, so that CTAs of
+    // consecutive kernels (programmatic dependent launch) can share an SM: the filter's
+    // two CTAs leave room for a refine CTA only if the SM is not configured smaller.
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
@@ -243,6 +271,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         const cudaError_t e = cudaLaunchKernelEx(&cfg, gvr_topk_cluster_kernel, scores, row_stride, row_lens, (int)k,
                                                  out_idx, out_val, stats, prm, prev_topk, phase_ts);
         mark(2);
+        mark(3);
         if (e != cudaSuccess) {
             g_last_cuda_error = e;
             (void)cudaGetLastError();
@@ -259,60 +288,134 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
                                                                       stats, prm, nullptr, nullptr, prev_topk, phase_ts,
                                                                       nullptr);
         mark(2);
+        mark(3);
         return launch_status();
     }
-    // Phase 1 for every row (one small CTA per row), then the streaming / refine kernel
-    // (one CTA per row, two CTAs per SM).  The per-row hand-off lives in the stream's
-    // cached scratch (acquire_scratch), so concurrent calls on different streams do not
-    // share it and steady-state calls allocate nothing.
-    // scratch: ctl[4] | GuessOut[num_rows] | order[num_rows].  ctl = {front cursor, back
-    // cursor, finished CTAs, 0} lives at a fixed offset and is zero between calls: the
-    // streaming kernel's last CTA resets it, so only a new buffer needs a memset.
+    // Batch path (more than one wave).  Phase 1 for every row (gvr_guess_kernel, one small
+    // CTA per row), then either
+    //  * the filter path (default): gvr_filter_kernel streams the whole
+    //    batch once (persistent, three CTAs per SM) into per-CTA candidate lists and queues
+    //    each row when its list is complete; gvr_refine_kernel (four small CTAs per SM)
+    //    selects every queued row from its list; the few rows it cannot finish are
+    //    streamed and refined by gvr_topk_kernel in fixup mode; or
+    //  * the row path (gvr_options.batch_path = 1): gvr_topk_kernel streams and refines one
+    //    row per CTA, two CTAs per SM.
+    // The kernels follow each other under programmatic dependent launch.  Scratch: the
+    // stream's cached lease (acquire_scratch).
+    CandLists cl{};
+    BatchQueue bq{};
+    bool filt = !(opt && opt->batch_path == 1);
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess || sms < 1) {
+        int dev = 0;
+        (void)cudaGetLastError();
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                       cudaSuccess) {
+            g_last_cuda_error = cudaGetLastError();
+            return GVR_ERR_CUDA;
+        }
+    }
+    // per-call arrays after the zero region: GuessOut[R] | order[R] | fixlist[R] |
+    // rec[R][F_SEGS] | region[G][reg]
     const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
-    const size_t scratch_bytes = 16 + gp_bytes + (size_t)num_rows * 4;
+    const size_t order_off = gp_bytes;
+    const size_t fix_off = order_off + (size_t)num_rows * 4;
+    const size_t rec_off = (fix_off + (size_t)num_rows * 4 + 255) & ~(size_t)255;
+    size_t after_bytes = fix_off;
+    size_t region_off = 0;
+    if (filt) {
+        const int tpr = (int)((row_stride + STAGE_FLOATS - 1) / STAGE_FLOATS);
+        const long long V = (long long)num_rows * tpr;
+        const int min_tiles = (tpr + 2) / 3;  // >= ceil(tpr / 3) tiles per CTA: <= F_SEGS CTAs per row
+        long long G = (long long)F_CTAS_PER_SM * sms;  // persistent: every filter CTA resident
+        if (G > V / min_tiles) G = V / min_tiles;
+        const long long per = (V + G - 1) / (G > 0 ? G : 1);
+        long long reg = per * STAGE_FLOATS / 8;  // room for 1/8 of the elements
+        if (reg < F_REG_MIN) reg = F_REG_MIN;
+        if (G < 1 || G * reg > 0x7fffffffLL) {
+            filt = false;
+        } else {
+            cl.V = V;
+            cl.G = (int)G;
+            cl.tpr = tpr;
+            cl.reg = (int)reg;
+            region_off = (rec_off + (size_t)num_rows * F_SEGS * sizeof(int4) + 255) & ~(size_t)255;
+            after_bytes = region_off + (size_t)G * (size_t)reg * sizeof(uint2);
+        }
+    }
+    if (filt && ((st = set_smem(gvr_filter_kernel, F_SMEM_BYTES)) != GVR_OK ||
+                 (st = set_smem(gvr_refine_kernel, RF_SMEM_BYTES)) != GVR_OK ||
+                 (st = set_smem(gvr_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK))
+        return st;
     ScratchLease lease;
-    if (acquire_scratch(stream, scratch_bytes, lease) != cudaSuccess) {
+    if (acquire_scratch(stream, num_rows, [&](int64_t) { return after_bytes; }, lease) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
     }
     unsigned char* scratch = lease.ptr;
+    unsigned char* per_call = scratch + zero_region_bytes(lease.rows_cap);
     int32_t* ctl = reinterpret_cast<int32_t*>(scratch);
-    GuessOut* gp = reinterpret_cast<GuessOut*>(scratch + 16);
-    RowSched sched{reinterpret_cast<int32_t*>(scratch + 16 + gp_bytes), ctl};
-    if (lease.fresh && cudaMemsetAsync(ctl, 0, 16, stream) != cudaSuccess) {
+    GuessOut* gp = reinterpret_cast<GuessOut*>(per_call);
+    RowSched sched{reinterpret_cast<int32_t*>(per_call + order_off), ctl};
+    if (filt) {
+        bq.qctl = reinterpret_cast<int32_t*>(scratch + 16);
+        bq.queue = bq.qctl + 4;
+        bq.segdone = bq.queue + lease.rows_cap;
+        bq.fixlist = reinterpret_cast<int32_t*>(per_call + fix_off);
+        cl.rec = reinterpret_cast<int4*>(per_call + rec_off);
+        cl.region = reinterpret_cast<uint2*>(per_call + region_off);
+    }
+    if (lease.fresh && cudaMemsetAsync(scratch, 0, zero_region_bytes(lease.rows_cap), stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         if (lease.temporary) (void)cudaFreeAsync(scratch, stream);
         return GVR_ERR_CUDA;
     }
+    // programmatic dependent launch: each kernel is scheduled while its predecessor runs
+    // (the refine CTAs become resident beside the filter CTAs); kernels that read their
+    // predecessor's output wait for it (griddepcontrol.wait) or for a per-row flag.
+    // Serialised when per-kernel events are recorded between them.
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = ev ? 0 : 1;
+    auto launch = [&](auto kern, int grid, int threads, int smem_bytes, auto... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.dynamicSmemBytes = (size_t)smem_bytes;
+        cfg.stream = stream;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, args...);
+    };
+    cudaError_t e = cudaSuccess;
     mark(0);
     gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm, gp,
-                                                        sched);
+                                                        sched, bq);
     mark(1);
-    {
-        // programmatic dependent launch: scheduled while the guess kernel runs, the
-        // streaming kernel waits for it (griddepcontrol.wait) before reading the hand-off;
-        // serialised when per-kernel events are recorded between the two
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)num_rows);
-        cfg.blockDim = dim3(GVR_NT);
-        cfg.dynamicSmemBytes = GVR_SMEM_BYTES;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = ev ? 0 : 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, gvr_topk_kernel, scores, row_stride, row_lens, (int)k, out_idx,
-                                                 out_val, stats, prm, static_cast<const GuessOut*>(gp),
-                                                 static_cast<const int32_t*>(sched.order),
-                                                 static_cast<const int32_t*>(nullptr), phase_ts, ctl);
-        if (e != cudaSuccess) {
-            g_last_cuda_error = e;
-            (void)cudaGetLastError();
-        }
+    const GuessOut* gpc = gp;
+    const int32_t* orderc = sched.order;
+    const int32_t* nop = nullptr;
+    if (filt) {
+        e = launch(gvr_filter_kernel, cl.G, F_NT, F_SMEM_BYTES, scores, row_stride, row_lens, (int)k, gpc, cl, bq);
+        mark(2);
+        if (e == cudaSuccess)
+            e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, scores,
+                       row_stride, row_lens, (int)k,
+                       (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts);
+        if (e == cudaSuccess)
+            e = launch(gvr_fixup_kernel, min((int)num_rows, sms), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
+                       (int)k, out_idx, out_val, stats, prm, gpc, prev_topk, phase_ts, ctl, bq);
+    } else {
+        e = launch(gvr_topk_kernel, (int)num_rows, GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens, (int)k, out_idx,
+                   out_val, stats, prm, gpc, orderc, nop, phase_ts, ctl);
+        mark(2);
     }
-    mark(2);
-    const gvr_status ls = launch_status();
+    if (e != cudaSuccess) {
+        g_last_cuda_error = e;
+        (void)cudaGetLastError();
+    }
+    mark(3);
+    const gvr_status ls = e != cudaSuccess ? GVR_ERR_CUDA : launch_status();
     if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;
@@ -331,10 +434,10 @@ gvr_status gvr_topk_batched_ex(const float* scores, int64_t row_stride, const in
 gvr_status gvr_topk_batched_events(const float* scores, int64_t row_stride, const int32_t* row_lens,
                                    int32_t num_rows, const int32_t* prev_topk, int32_t k, int32_t* out_idx,
                                    cudaStream_t stream, cudaEvent_t guess_start, cudaEvent_t stream_start,
-                                   cudaEvent_t stream_end)
+                                   cudaEvent_t stream_end, cudaEvent_t call_end, const gvr_options* opt)
 {
-    const cudaEvent_t ev[3] = {guess_start, stream_start, stream_end};
-    return gvr_launch(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, nullptr, nullptr, nullptr,
+    const cudaEvent_t ev[4] = {guess_start, stream_start, stream_end, call_end};
+    return gvr_launch(scores, row_stride, row_lens, num_rows, prev_topk, k, out_idx, stream, opt, nullptr, nullptr,
                       nullptr, ev);
 }
 

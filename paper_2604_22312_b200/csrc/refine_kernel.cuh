@@ -1,0 +1,357 @@
+// refine_kernel.cuh — the batch path's refine step: Phase 4 and the ordered output from the
+// candidate lists gvr_filter_kernel leaves in L2.
+//
+// A persistent grid of four small CTAs per SM (29 KB of shared memory, <= 64 registers)
+// launched behind the filter with programmatic dependent launch: one wave covers a decode
+// batch, and CTAs that find room early start on the rows already complete.  CTAs pop rows
+// from the ready queue in the // order their lists complete.  Per row (all of it exact key-space arithmetic):
+//   * the row's <= F_SEGS list segments and their largest keys (filter records);
+//   * Phase 4 fused with the ordered output (R28), over the
+//     list itself, read from L2: a 2048-bin linear histogram of the keys >= T_c over
+//     [T_c, kmax] (bin 0 = highest), the bin holding sorted position K-1 from the bin scan,
+//     the entries of the bins up to it counting-sorted into shared memory as 64-bit
+//     composites (key, ~index), each ranked inside its bin, and position j < K written to
+//     out[j] — score descending, index ascending;
+//   * rows this cannot finish — no tiles (len <= k or tiny rows), a list that overflowed its
+//     region or holds fewer than K keys >= T_c (the guess overshot), a K-th bin crowded by
+//     ties — go to the fixup list, worked off by gvr_topk_kernel in fixup mode.
+// The paper's Phase 2 (secant narrowing to C candidates) exists to fit
+// the candidates in shared memory; here the list stays in L2 and the histogram covers it
+// directly, so f(T_c) is the only count (secant_iters = 1).
+#pragma once
+#include "filter_kernel.cuh"
+
+namespace gvr {
+
+constexpr int RF_NT = 256;
+constexpr int RF_CSORT = 2560;     // entries up to the K-th bin sorted in shared memory
+constexpr int RF_MAXLIST = 65535;  // bin counts and cursors are 16-bit
+constexpr int RF_BIN_FAST = 16;    // largest bin ranked without narrowing first
+using RefineGroup = Group<RF_NT, 1>;
+constexpr int RF_OFF_HIST = 0;                       // u16 bin counts, two per word
+constexpr int RF_OFF_CUR = RF_OFF_HIST + NBINS * 2;  // u16 bin cursors, two per word
+constexpr int RF_OFF_CS = RF_OFF_CUR + NBINS * 2;
+constexpr int RF_OFF_ROW = RF_OFF_CS + RF_CSORT * 8;
+constexpr int RF_OFF_SCR = RF_OFF_ROW + 16;
+constexpr int RF_SMEM_BYTES = RF_OFF_SCR + GROUP_SCRATCH_BYTES;
+constexpr int RF_CTAS_PER_SM = 4;  // one wave for a decode batch: the per-row work is latency bound
+static_assert(RF_CTAS_PER_SM * (RF_SMEM_BYTES + 1024) <= 233472, "four refine CTAs per SM");
+
+// 16-bit counters packed two per 32-bit word (shared memory)
+__device__ __forceinline__ int h16_get(const uint32_t* w, int b) { return (int)((w[b >> 1] >> ((b & 1) * 16)) & 0xffffu); }
+__device__ __forceinline__ int h16_add(uint32_t* w, int b)
+{
+    const int sh = (b & 1) * 16;
+    return (int)((atomicAdd(&w[b >> 1], 1u << sh) >> sh) & 0xffffu);
+}
+
+// Entries q0, q0 + stride, ... of the row's list (segment s: entries [cum[s], cum[s+1]) at
+// region[gs[s] + q - cum[s]], read through L2), or of the row itself when rowx != nullptr.
+// Keys only (the histogram passes): entries q0, q0 + stride, ... as list_load.
+template <int UNR>
+__device__ __forceinline__ void list_keys(const CandLists& cl, const float* rowx, const int (&gs)[F_SEGS],
+                                          const int (&cum)[F_SEGS + 1], int total, int q0, int stride, uint32_t (&kv)[UNR])
+{
+    const uint32_t* rk = reinterpret_cast<const uint32_t*>(cl.region);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        const int q = q0 + u * stride;
+        if (rowx) {
+            kv[u] = q < total ? f2key(__ldg(rowx + q)) : 0u;
+            continue;
+        }
+        int s = 0;
+#pragma unroll
+        for (int v = 1; v < F_SEGS; ++v) s += q >= cum[v];
+        const int base = s == 0 ? gs[0] : s == 1 ? gs[1] : s == 2 ? gs[2] : gs[3];
+        const int c0 = s == 0 ? cum[0] : s == 1 ? cum[1] : s == 2 ? cum[2] : cum[3];
+        kv[u] = q < total ? __ldcg(rk + 2 * (size_t)(base + (q - c0))) : 0u;
+    }
+}
+
+template <int UNR>
+__device__ __forceinline__ void list_load(const CandLists& cl, const float* rowx, const int (&gs)[F_SEGS],
+                                          const int (&cum)[F_SEGS + 1], int total, int q0, int stride, uint2 (&e)[UNR])
+{
+    if (rowx) {  // a row with len <= k is its own list: (key, position)
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int q = q0 + u * stride;
+            e[u] = q < total ? make_uint2(f2key(__ldg(rowx + q)), (uint32_t)q) : make_uint2(0u, 0u);
+        }
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        const int q = q0 + u * stride;
+        int s = 0;
+#pragma unroll
+        for (int v = 1; v < F_SEGS; ++v) s += q >= cum[v];
+        const int base = s == 0 ? gs[0] : s == 1 ? gs[1] : s == 2 ? gs[2] : gs[3];
+        const int c0 = s == 0 ? cum[0] : s == 1 ? cum[1] : s == 2 ? cum[2] : cum[3];
+        e[u] = q < total ? __ldcg(cl.region + base + (q - c0)) : make_uint2(0u, 0u);
+    }
+}
+
+__global__ void __launch_bounds__(RF_NT, RF_CTAS_PER_SM)
+gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
+                  int num_rows, int32_t* out, float* out_val, gvr_row_stats* stats, const GuessOut* gp, CandLists cl,
+                  BatchQueue bq, long long* phase_ts)
+{
+    // phase_ts (optional, [num_rows][TS_N]): clock64 at the pop, after the segment records,
+    // after the histogram pass, after the K-th bin search, after the scatter, at the end;
+    // then globaltimer at the pop and the end, and the SM id.
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + RF_OFF_HIST);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(smem + RF_OFF_CUR);
+    unsigned long long* cs = reinterpret_cast<unsigned long long*>(smem + RF_OFF_CS);
+    int* sh_row = reinterpret_cast<int*>(smem + RF_OFF_ROW);
+    RefineGroup c;
+    c.init(threadIdx.x, smem + RF_OFF_SCR);
+    const int K = k;
+    constexpr int BPT = NBINS / RF_NT;
+    constexpr int UNR = 8;
+    for (;;) {
+        if (c.tid == 0) {
+            const int slot = atomicAdd(bq.qctl + Q_HEAD, 1);
+            int r = -1;
+            if (slot < num_rows) {
+                int v;
+                while ((v = ld_acquire(bq.queue + slot)) == 0) __nanosleep(100);
+                r = v - 1;
+                bq.queue[slot] = 0;
+            }
+            *sh_row = r;
+        }
+        c.sync();
+        const int r = *sh_row;
+        if (r < 0) break;
+        long long tsr[TS_N] = {phase_ts ? clock64() : 0ll, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
+        const RowPlan p = plan_row(scores, stride, row_lens, r, k);
+        // ---- the row's list segments (filter records)
+        int total = -1;
+        uint32_t kmax = 0u;
+        if (p.ntiles > 0 && c.warp == 0) {
+            const long long v0 = (long long)r * cl.tpr;
+            const int b0 = cl_cta_of(cl, v0);
+            const int ns = cl_cta_of(cl, v0 + p.ntiles - 1) - b0 + 1;
+            int gsv = 0, n = 0, bad = ns > F_SEGS ? 1 : 0;
+            uint32_t km = 0u;
+            if (c.lane < ns && c.lane < F_SEGS) {
+                const int4 e = __ldcg(cl.rec + (long long)r * F_SEGS + c.lane);
+                bad = (e.x != b0 + c.lane || e.y < 0 || e.z < e.y || e.z > cl.reg) ? 1 : 0;
+                gsv = e.x * cl.reg + e.y;
+                n = e.z - e.y;
+                km = (uint32_t)e.w;
+            }
+            bad = __any_sync(FULL, bad);
+            const int tot = (int)__reduce_add_sync(FULL, (uint32_t)n);
+            km = __reduce_max_sync(FULL, km);
+            if (c.lane < F_SEGS) {
+                c.misc[24 + 2 * c.lane] = gsv;
+                c.misc[25 + 2 * c.lane] = n;
+            }
+            if (c.lane == 0) {
+                c.misc[22] = bad ? -1 : tot;
+                c.misc[23] = (int)km;
+                bq.segdone[r] = 0;  // popped: reset for the next call
+            }
+        }
+        c.sync();
+        int gs[F_SEGS], cum[F_SEGS + 1];
+        if (p.ntiles > 0) {
+            total = c.misc[22];
+            kmax = (uint32_t)c.misc[23];
+            cum[0] = 0;
+#pragma unroll
+            for (int s = 0; s < F_SEGS; ++s) {
+                gs[s] = c.misc[24 + 2 * s];
+                cum[s + 1] = cum[s] + c.misc[25 + 2 * s];
+            }
+        }
+        uint32_t Tc = __ldcg(&gp[r].Tc);
+        bool ok = p.ntiles > 0 && p.n > k && total >= K && total <= RF_MAXLIST && kmax >= Tc;
+        // a row with len <= k: every element is selected (take = len), binned over its own
+        // key range [min, max], then -1 padding (R5)
+        const bool trivial = p.n <= k;
+        const float* rowx = nullptr;
+        int take = K;
+        if (trivial) {
+            uint32_t mn = 0xffffffffu, mx2 = 0u;
+            for (int q = c.tid; q < p.n; q += RF_NT) {
+                const uint32_t kv = f2key(__ldg(p.x + q));
+                mn = min(mn, kv);
+                mx2 = max(mx2, kv);
+            }
+            group_red2<R_MIN, R_MAX>(c, mn, mx2);
+            rowx = p.x;
+            total = p.n;
+            take = p.n;
+            Tc = mn;
+            kmax = mx2;
+            ok = p.n > 0;
+        }
+        if (phase_ts) tsr[TS_PHASE1] = clock64();
+        int ftc = 0, nsel = 0;
+        if (ok) {
+            // ---- Phase 4: histogram of the keys >= lo over [lo, kmax],
+            // the K-th bin from the bin scan.  lo starts at T_c; if the
+            // bins up to the K-th one are too crowded to rank (keys spread over a wide key
+            // range, e.g. both signs, leave the top K in few linear bins), lo is raised to
+            // the K-th bin's lower edge and the histogram redone over the narrower range
+            // (every key >= lo still holds the first `take` positions).
+            uint32_t lo = Tc, scale = 0u, off0 = 0u;
+            const int b0 = c.tid * BPT;
+            int h[BPT];
+            int bk = -1;
+            for (int lvl = 0; lvl < 3; ++lvl) {
+                for (int i = c.tid; i < NBINS / 2; i += RF_NT) hist[i] = 0u;
+                if (c.tid == 0) c.misc[12] = -1;  // K-th bin: set below by the thread that holds it
+                c.sync();
+                scale = bin_scale((uint64_t)kmax - lo + 1ull);
+                uint32_t f = 0;
+                constexpr int UK = 16;
+                for (int q0 = c.tid; q0 < total; q0 += UK * RF_NT) {
+                    uint32_t kv[UK];
+                    list_keys<UK>(cl, rowx, gs, cum, total, q0, RF_NT, kv);
+#pragma unroll
+                    for (int u = 0; u < UK; ++u)
+                        if (q0 + u * RF_NT < total && kv[u] >= lo) {
+                            h16_add(hist, (NBINS - 1) - lin_bin(kv[u] - lo, scale));
+                            ++f;
+                        }
+                }
+                f = group_red1<R_ADD>(c, f);  // its barrier also completes the histogram
+                if (lvl == 0) {
+                    ftc = (int)f;
+                    if (phase_ts) tsr[TS_STREAM] = clock64();
+                }
+                uint32_t loc = 0;
+#pragma unroll
+                for (int i = 0; i < BPT; ++i) {
+                    h[i] = h16_get(hist, b0 + i);
+                    loc += (uint32_t)h[i];
+                }
+                uint32_t tot;
+                off0 = group_excl_scan(c, loc, tot);
+                {
+                    uint32_t off = off0;
+#pragma unroll
+                    for (int i = 0; i < BPT; ++i) {
+                        if ((uint32_t)(take - 1) >= off && (uint32_t)(take - 1) < off + (uint32_t)h[i]) {
+                            c.misc[12] = b0 + i;
+                            c.misc[13] = (int)(off + (uint32_t)h[i]);
+                        }
+                        off += (uint32_t)h[i];
+                    }
+                }
+                c.sync();
+                bk = ftc >= take ? c.misc[12] : -1;
+                nsel = c.misc[13];
+                uint32_t mx = 0;
+#pragma unroll
+                for (int i = 0; i < BPT; ++i)
+                    if (b0 + i <= bk) mx = max(mx, (uint32_t)h[i]);
+                mx = group_red1<R_MAX>(c, mx);
+                ok = bk >= 0 && nsel <= RF_CSORT && mx <= (uint32_t)CSORT_BIN_MAX;  // group-uniform
+                // narrow also when the ranking would loop over bins of more than RF_BIN_FAST
+                if (bk < 0 || lvl == 2 || (ok && mx <= (uint32_t)RF_BIN_FAST)) break;
+                // lower edge of bin bk: the smallest d with lin_bin(d) = NBINS - 1 - bk
+                const uint64_t L = (uint64_t)(NBINS - 1 - bk);
+                const uint64_t dmin = ((L << 32) + scale - 1ull) / scale;
+                if (dmin == 0ull) break;  // the K-th bin is the lowest: narrowing cannot help
+                lo += (uint32_t)dmin;
+            }
+            if (phase_ts) tsr[TS_PHASE23] = clock64();
+            if (ok) {
+                {
+                    uint32_t off = off0;
+#pragma unroll
+                    for (int i = 0; i < BPT; i += 2) {
+                        // bin starts (two per word); they become the bin ends after the scatter
+                        cur[(b0 + i) >> 1] = off | ((off + (uint32_t)h[i]) << 16);
+                        off += (uint32_t)h[i] + (uint32_t)h[i + 1];
+                    }
+                }
+                c.sync();
+                // ---- counting sort of the bins up to the K-th bin (composites)
+                for (int q0 = c.tid; q0 < total; q0 += UNR * RF_NT) {
+                    uint2 e[UNR];
+                    list_load<UNR>(cl, rowx, gs, cum, total, q0, RF_NT, e);
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u)
+                        if (q0 + u * RF_NT < total && e[u].x >= lo) {
+                            const int b = (NBINS - 1) - lin_bin(e[u].x - lo, scale);
+                            if (b <= bk) cs[h16_add(cur, b)] = make_comp(e[u].x, (int32_t)e[u].y);
+                        }
+                }
+                c.sync();
+                if (phase_ts) tsr[TS_PHASE4] = clock64();
+                // ---- rank inside the bin; positions < K are the ordered output
+                int32_t* o = out + (int64_t)r * k;
+                float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
+                for (int j = c.tid; j < nsel; j += RF_NT) {
+                    const unsigned long long v = cs[j];
+                    const int b = (NBINS - 1) - lin_bin(comp_key(v) - lo, scale);
+                    const int cnt = h16_get(hist, b);
+                    const int st = h16_get(cur, b) - cnt;
+                    const int wmax = (int)__reduce_max_sync(__activemask(), (uint32_t)cnt);
+                    int rank = 0;
+                    if (wmax <= 4) {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (t < cnt) rank += cs[st + t] > v;
+                    } else if (wmax <= 8) {
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            if (t < cnt) rank += cs[st + t] > v;
+                    } else {
+                        for (int i2 = st; i2 < st + cnt; ++i2) rank += cs[i2] > v;
+                    }
+                    const int pos = st + rank;
+                    if (pos < take) {
+                        o[pos] = comp_idx(v);
+                        if (ov) ov[pos] = key2f(comp_key(v));
+                    }
+                }
+                for (int j = take + c.tid; j < k; j += RF_NT) {  // len < k: -1 padding
+                    o[j] = -1;
+                    if (ov) ov[j] = 0.f;
+                }
+            }
+        }
+        if (trivial && p.n == 0) {
+            int32_t* o = out + (int64_t)r * k;
+            for (int j = c.tid; j < k; j += RF_NT) {
+                o[j] = -1;
+                if (out_val) out_val[(int64_t)r * k + j] = 0.f;
+            }
+            ok = true;
+        }
+        if (c.tid == 0) {
+            if (!ok) {
+                bq.fixlist[atomicAdd(bq.qctl + Q_NFIX, 1)] = r;
+            } else if (stats) {
+                gvr_row_stats s;
+                s.secant_iters = trivial ? 0 : 1;  // f(T_c), counted from the list
+                s.snap_iters = 0;
+                s.cand_count = trivial ? p.n : ftc;
+                s.done_kind = trivial ? GVR_DONE_TRIVIAL : GVR_DONE_CONVERGED;
+                s.global_passes = 1;
+                s.raises = 0;
+                s.buffer_count = trivial ? 0 : ftc;
+                s.cluster = 1;
+                stats[r] = s;
+            }
+            if (phase_ts && ok) {
+                tsr[TS_END] = clock64();
+                tsr[TS_GEND] = global_ns();
+                tsr[TS_SMID] = sm_id();
+                for (int i = 0; i < TS_N; ++i) phase_ts[(int64_t)r * TS_N + i] = tsr[i];
+            }
+        }
+        c.sync();  // smem (row slot, histogram, sort buffer) is reused for the next row
+    }
+}
+
+}  // namespace gvr

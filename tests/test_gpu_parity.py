@@ -171,9 +171,11 @@ def test_in_place_prev_equals_out(gvr):
 
 
 # ------------------------------------------------------------------ full-size config
-def test_full_size_cfg2_batch(gvr):
+@pytest.mark.parametrize("path", [0, 1])
+def test_full_size_cfg2_batch(gvr, path):
     """BASELINE.json configs[1]: 8 requests x 61 layers at N=100K, prev-step guesses,
-    in the launch configuration bench.py times (one launch over all 488 rows)."""
+    in the launch configuration bench.py times (one call over all 488 rows), on the
+    filter path (0, the default) and the row path (1)."""
     import torch
     from bench import make_decode_batch
     dev = torch.device("cuda:0")
@@ -182,7 +184,8 @@ def test_full_size_cfg2_batch(gvr):
     host = batch["scores"].cpu().numpy()
     lens = batch["row_lens"].cpu().numpy()
     ref = oracle.topk_batched(host, K, row_lens=lens)
-    out = gvr.topk(batch["scores"], K, row_lens=batch["row_lens"], prev=batch["prev"])
+    out = gvr.topk(batch["scores"], K, row_lens=batch["row_lens"], prev=batch["prev"],
+                   options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
     rad = gvr.radix_topk(batch["scores"], K, row_lens=batch["row_lens"])
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref)
@@ -283,12 +286,26 @@ def test_events_entry_point(gvr):
     import torch
     dev = torch.device("cuda:0")
     host, lens, prev = _decode_rows(4, seed=450)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     out = gvr.topk_events(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
                           prev=torch.from_numpy(prev).to(dev), events=evs)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
-    assert evs[0].elapsed_time(evs[1]) > 0 and evs[1].elapsed_time(evs[2]) > 0
+    assert evs[0].elapsed_time(evs[1]) >= 0 and evs[1].elapsed_time(evs[2]) > 0
+    assert evs[2].elapsed_time(evs[3]) >= 0
+
+
+def test_events_entry_point_filter_path(gvr):
+    """More than one wave: the four events bracket the guess, filter and refine kernels."""
+    import torch
+    dev = torch.device("cuda:0")
+    host, lens, prev = _decode_rows(300, n=12_000, seed=460)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    out = gvr.topk_events(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
+                          prev=torch.from_numpy(prev).to(dev), events=evs)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
+    assert all(evs[i].elapsed_time(evs[i + 1]) > 0 for i in range(3))
 
 
 # ------------------------------------------------------------------ cluster per row
@@ -407,10 +424,11 @@ def test_guess_overshoot_takes_a_second_pass(gvr, n):
             assert (st[:, 4] == 2).all() and (st[:, 3] == 1).all(), st.tolist()  # two passes, converged
 
 
-def test_split_path_ragged_trivial_and_mixed_guesses(gvr):
-    """More than one wave of rows (guess kernel + streaming kernel with row scheduling):
-    ragged lengths including empty and len <= k rows, every guess kind, value
-    distributions; exact against the oracle."""
+@pytest.mark.parametrize("path", [0, 1])
+def test_split_path_ragged_trivial_and_mixed_guesses(gvr, path):
+    """More than one wave of rows (guess kernel, then the filter + refine kernels (path 0)
+    or the row streaming kernel (path 1)): ragged lengths including empty and len <= k
+    rows, every guess kind, value distributions; exact against the oracle."""
     import torch
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(11)
@@ -432,8 +450,142 @@ def test_split_path_ragged_trivial_and_mixed_guesses(gvr):
             prev[r] = g
     ref = oracle.topk_batched(host, K, row_lens=lens)
     out = gvr.topk(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
-                   prev=torch.from_numpy(prev).to(dev))
+                   prev=torch.from_numpy(prev).to(dev), options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
     torch.cuda.synchronize()
     got = out.cpu().numpy()
     bad = np.argwhere((got != ref).any(axis=1))[:, 0]
     assert bad.size == 0, f"{bad.size} rows differ, first {bad[:5].tolist()} lens {lens[bad[:5]].tolist()}"
+
+
+def _filter_batch(gvr, host, lens, prev, k=K, path=0):
+    import torch
+    dev = torch.device("cuda:0")
+    p = None if prev is None else torch.from_numpy(np.ascontiguousarray(prev, np.int32)).to(dev)
+    idx, val, st = gvr.topk_ex(torch.from_numpy(host).to(dev), k, row_lens=torch.from_numpy(lens).to(dev), prev=p,
+                               options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), val.cpu().numpy(), st.cpu().numpy()
+
+
+def _assert_rows(got, ref, lens, st=None):
+    bad = np.argwhere((got != ref).any(axis=1))[:, 0]
+    assert bad.size == 0, (f"{bad.size} rows differ, first {bad[:5].tolist()} lens {lens[bad[:5]].tolist()}"
+                           + ("" if st is None else f" stats {st[bad[:3]].tolist()}"))
+
+
+@pytest.mark.parametrize("stride_pad", [0, 1, 2, 3, 5])
+def test_filter_path_misaligned_rows(gvr, stride_pad):
+    """Filter path with row strides that are not a multiple of 4 floats: every row has its
+    own unaligned head and tail scalars, handled in the rounds holding its first and last
+    tiles; some rows span several filter CTAs."""
+    R, n = 320, 30_000 + stride_pad
+    rows = [synth.dist_row(synth.DISTRIBUTIONS[r % len(synth.DISTRIBUTIONS)], n - (r % 4), seed=1000 + r)
+            for r in range(R)]
+    host, lens = _pack(rows, stride=n)
+    prev = np.full((R, K), -1, np.int32)
+    for r in range(R):
+        g = synth.guess(synth.GUESS_KINDS[r % len(synth.GUESS_KINDS)], rows[r], K, 1001 + r,
+                        prev_topk=oracle.topk(rows[r], K))
+        if g is not None:
+            prev[r] = g
+    ref = oracle.topk_batched(host, K, row_lens=lens)
+    got, val, st = _filter_batch(gvr, host, lens, prev)
+    _assert_rows(got, ref, lens, st)
+    for r in range(0, R, 17):
+        m = min(K, lens[r])
+        assert np.array_equal(val[r, :m].view(np.uint32), host[r, ref[r, :m]].view(np.uint32))
+
+
+@pytest.mark.parametrize("k", [1, 7, 100, 1000, 2047])
+def test_filter_path_small_k(gvr, k):
+    R, n = 310, 9_000
+    rows = [synth.dist_row("normal", n, seed=1100 + r) for r in range(R)]
+    host, lens = _pack(rows)
+    ref = oracle.topk_batched(host, k, row_lens=lens)
+    prev = np.stack([oracle.topk(synth.dist_row("normal", n, seed=1100 + r + 1), k) for r in range(R)])
+    got, _, st = _filter_batch(gvr, host, lens, prev, k=k)
+    _assert_rows(got, ref, lens, st)
+
+
+def test_filter_path_poor_guesses_and_long_lists(gvr):
+    """Rows whose guess says nothing (rho = 0, layers 0-1 of DSV3.2): the guess kernel takes
+    the threshold from a row sample; rows whose list exceeds the shared-memory buffer are
+    cut by the count search; rows with massive ties or overflowing lists are streamed
+    again by the refine kernel.  Exact in every case, with stats consistent."""
+    R, n = 300, 100_000
+    rows, prevs = [], []
+    for r in range(R):
+        kind = r % 5
+        if kind == 0:
+            p, c = synth.decode_pair(n, 0.0, seed=1200 + r)
+            rows.append(c.numpy())
+            prevs.append(oracle.topk(p.numpy(), K))
+        elif kind == 1:
+            p, c = synth.decode_pair(n, 0.9, seed=1200 + r)
+            rows.append(c.numpy())
+            prevs.append(oracle.topk(p.numpy(), K))
+        elif kind == 2:
+            row = synth.dist_row(("few_distinct", "all_equal", "ties90")[(r // 5) % 3], n, seed=1200 + r)
+            rows.append(row)
+            prevs.append(synth.guess("random", row, K, 1201 + r))
+        elif kind == 3:
+            row = synth.dist_row("normal", n, seed=1200 + r)
+            rows.append(row)
+            prevs.append(synth.guess("adversarial", row, K, 1201 + r, prev_topk=oracle.topk(row, K)))
+        else:
+            row = synth.dist_row("normal", n, seed=1200 + r)
+            rows.append(row)
+            prevs.append(None)
+    prev = np.stack([p if p is not None else np.full(K, -1, np.int32) for p in prevs])
+    host, lens = _pack(rows)
+    ref = oracle.topk_batched(host, K, row_lens=lens)
+    got, _, st = _filter_batch(gvr, host, lens, prev)
+    _assert_rows(got, ref, lens, st)
+    assert (st[:, 4] >= 1).all()  # global passes
+    good = st[1::5]
+    assert (good[:, 4] == 1).all() and (good[:, 3] == 1).all(), good[:5].tolist()  # one pass, converged
+
+
+def test_filter_path_cuda_graph(gvr):
+    """The three-kernel filter path (guess, filter, refine) and its scratch capture into a
+    CUDA graph; replays on new inputs written into the same buffers are exact."""
+    import torch
+    dev = torch.device("cuda:0")
+    host_a, lens, prev_a = _decode_rows(300, n=12_000, seed=1300)
+    host_b, _, prev_b = _decode_rows(300, n=12_000, seed=1400)
+    s = torch.from_numpy(host_a).to(dev)
+    l = torch.from_numpy(lens).to(dev)
+    p = torch.from_numpy(prev_a).to(dev)
+    out = torch.empty((300, K), dtype=torch.int32, device=dev)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        gvr.topk(s, K, row_lens=l, prev=p, out=out)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        gvr.topk(s, K, row_lens=l, prev=p, out=out)
+    for host, prev in ((host_a, prev_a), (host_b, prev_b)):
+        s.copy_(torch.from_numpy(host))
+        p.copy_(torch.from_numpy(prev))
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
+
+
+def test_filter_and_row_paths_agree_on_cfg4(gvr):
+    """BASELINE.json configs[3] shape (MTP: 4 draft rows per request, N + j keys) at 16
+    requests x 8 layers: both batch paths equal the oracle."""
+    import torch
+    from bench import make_decode_batch
+    dev = torch.device("cuda:0")
+    batch = make_decode_batch(16, 8, 100_000, dev, seed=synth.BASE_SEED + 7, draft=4)
+    torch.cuda.synchronize()
+    host = batch["scores"].cpu().numpy()
+    lens = batch["row_lens"].cpu().numpy()
+    ref = oracle.topk_batched(host, K, row_lens=lens)
+    for path in (0, 1):
+        out = gvr.topk(batch["scores"], K, row_lens=batch["row_lens"], prev=batch["prev"],
+                       options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
+        torch.cuda.synchronize()
+        _assert_rows(out.cpu().numpy(), ref, lens)
