@@ -14,7 +14,7 @@
 // give every lane its write positions (ballot-free), and the writes go
 // straight from the lanes to L2, with no shared staging and no global atomics.  At the end
 // of each row segment the CTA records (cta, start, end) of that row's entries in its
-// region; the refine step (gvr_topk_kernel in candidate mode) gathers a row's <= F_SEGS
+// region; the refine step (gvr_refine_kernel) gathers a row's <= F_SEGS
 // segments, and Lemma 1 makes {key >= T_c} enough for the exact Top-K
 // whenever it holds at least K entries.
 #pragma once
@@ -68,6 +68,19 @@ struct RoundIter {
     }
 };
 
+// Candidate store with an L2 evict-last hint: the lists are re-read by the refine kernel
+// right after the stream, whose own tiles are loaded evict-first.
+__device__ __forceinline__ void st_cand(uint2* p, uint32_t key, uint32_t idx, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(key), "r"(idx), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void issue_tile(const Ring& ring, const RowPlan& p, int t, int s)
 {
     const uint32_t bytes = (uint32_t)min(STAGE_FLOATS, p.nfl - t * STAGE_FLOATS) * 4u;
@@ -117,6 +130,7 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     c.sync();
     uint2* reg = cl.region + (long long)b * cl.reg;
     const int regcap = cl.reg;
+    const uint64_t keep = policy_evict_last();
     RoundIter it;
     it.v = vb;
     it.ve = ve;
@@ -173,14 +187,14 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             const int o = rel_off(e);
             const uint32_t u = __float_as_uint(sp[lb + o]);
             const uint32_t kv = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);  // f2key
-            if (pos < regcap) reg[pos] = make_uint2(kv, (uint32_t)(ibase + o));
+            if (pos < regcap) st_cand(reg + pos, kv, (uint32_t)(ibase + o), keep);
             kmax = max(kmax, kv);
             ++pos;
         }
         if (si >= 0 && pass_ge(sv, Tf)) {
             const int q = atomicAdd(cursor, 1);
             const uint32_t kv = f2key(sv);
-            if (q < regcap) reg[q] = make_uint2(kv, (uint32_t)(p.idx0 + si));
+            if (q < regcap) st_cand(reg + q, kv, (uint32_t)(p.idx0 + si), keep);
             kmax = max(kmax, kv);
         }
         if (it.last) {

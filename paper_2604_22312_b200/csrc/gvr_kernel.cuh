@@ -756,6 +756,9 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     GuessGroup c;
     c.init(threadIdx.x, scratch);
     const int r = blockIdx.x;
+    // the guess indices do not depend on the row length: start fetching them into L2 now
+    if (prev && c.tid < (k + 31) / 32)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(prev + (int64_t)r * k + 32 * c.tid));
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
     // batch filter path: a row with no tiles never reaches the filter kernel; it goes to
     // the ready queue now (the refine kernel hands it on to the fixup list)

@@ -35,7 +35,7 @@ constexpr int RF_OFF_ROW = RF_OFF_CS + RF_CSORT * 8;
 constexpr int RF_OFF_SCR = RF_OFF_ROW + 16;
 constexpr int RF_SMEM_BYTES = RF_OFF_SCR + GROUP_SCRATCH_BYTES;
 constexpr int RF_CTAS_PER_SM = 4;  // one wave for a decode batch: the per-row work is latency bound
-static_assert(RF_CTAS_PER_SM * (RF_SMEM_BYTES + 1024) <= 233472, "four refine CTAs per SM");
+static_assert(RF_CTAS_PER_SM * (RF_SMEM_BYTES + 1024) <= 233472, "refine CTAs per SM");
 
 // 16-bit counters packed two per 32-bit word (shared memory)
 __device__ __forceinline__ int h16_get(const uint32_t* w, int b) { return (int)((w[b >> 1] >> ((b & 1) * 16)) & 0xffffu); }
@@ -127,6 +127,11 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         const int r = *sh_row;
         if (r < 0) break;
         long long tsr[TS_N] = {phase_ts ? clock64() : 0ll, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
+        // the segment records, the row length and T_c are loaded together (the records of
+        // slots past the row's segment count are stale and ignored)
+        const int4 erec = c.warp == 0 && c.lane < F_SEGS ? __ldcg(cl.rec + (long long)r * F_SEGS + c.lane)
+                                                         : make_int4(0, 0, 0, 0);
+        uint32_t Tc = __ldcg(&gp[r].Tc);
         const RowPlan p = plan_row(scores, stride, row_lens, r, k);
         // ---- the row's list segments (filter records)
         int total = -1;
@@ -138,7 +143,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             int gsv = 0, n = 0, bad = ns > F_SEGS ? 1 : 0;
             uint32_t km = 0u;
             if (c.lane < ns && c.lane < F_SEGS) {
-                const int4 e = __ldcg(cl.rec + (long long)r * F_SEGS + c.lane);
+                const int4 e = erec;
                 bad = (e.x != b0 + c.lane || e.y < 0 || e.z < e.y || e.z > cl.reg) ? 1 : 0;
                 gsv = e.x * cl.reg + e.y;
                 n = e.z - e.y;
@@ -169,7 +174,6 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 cum[s + 1] = cum[s] + c.misc[25 + 2 * s];
             }
         }
-        uint32_t Tc = __ldcg(&gp[r].Tc);
         bool ok = p.ntiles > 0 && p.n > k && total >= K && total <= RF_MAXLIST && kmax >= Tc;
         // a row with len <= k: every element is selected (take = len), binned over its own
         // key range [min, max], then -1 padding (R5)
