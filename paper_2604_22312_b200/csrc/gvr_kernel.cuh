@@ -712,8 +712,9 @@ struct RowSched {
 
 constexpr int SQ_N = 1024;  // row samples for the threshold of a poor-guess row
 
-// The rank-th largest of the SQ_N keys in sq (1 <= rank <= SQ_N): most-significant-digit
+// The rank-th largest of the NS keys in sq (1 <= rank <= NS): most-significant-digit
 // radix select, 8 bits per level over a 256-bin histogram (one bin per thread).
+template <int NS>
 __device__ __forceinline__ uint32_t sample_rank_key(GuessGroup& c, const uint32_t* sq, int32_t* sh, int rank)
 {
     uint32_t prefix = 0u, pmask = 0u, rem = (uint32_t)rank;
@@ -723,7 +724,7 @@ __device__ __forceinline__ uint32_t sample_rank_key(GuessGroup& c, const uint32_
         sh[c.tid] = 0;
         c.sync();
 #pragma unroll
-        for (int j = 0; j < SQ_N / GUESS_NT; ++j) {
+        for (int j = 0; j < NS / GUESS_NT; ++j) {
             const uint32_t kk = sq[c.tid + j * GUESS_NT];
             if ((kk & pmask) == prefix) atomicAdd(&sh[(kk >> shift) & 255u], 1);
         }
@@ -774,20 +775,31 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     const uint32_t hits = group_red1<R_ADD>(c, f2key(xs) >= g.Tc ? 1u : 0u);
     const bool heavy = (double)hits * p.n > (double)GVR_CAP * GUESS_NT;  // estimated f(T_c) > capacity
     if (heavy && p.n >= 4 * k) {
-        // poor guess (low Top-K overlap, e.g. layers 0-1): its statistics
-        // put T_c far below the K-th value.  Take the threshold from a strided sample of
-        // SQ_N row values instead: the r-th largest sample key, r chosen so that about
-        // f_s = 2.5 k + 512 elements are expected at or above it (sampling error of
-        // f(T_s)/f_s ~ 1/sqrt(r); an undershoot only costs the row a second stream).
+        // poor guess (low Top-K overlap, e.g. layers 0-1, or late MTP
+        // draft tokens): its statistics put T_c below the K-th value by more than the
+        // buffer.  Take the threshold from strided row samples instead: the r-th largest
+        // sample key, r chosen so that about f_s elements are expected at or above it
+        // (sampling error of f(T_s)/f_s ~ 1/sqrt(r); an undershoot only costs the row a
+        // second stream).  Far above the buffer (estimate > 4x): 1024 new samples and
+        // f_s = 2.5 k + 512; otherwise the 256 samples already gathered (no second round
+        // trip) and a safer f_s = 4 k.
         __shared__ uint32_t sq[SQ_N];
         __shared__ int32_t sh[GUESS_NT];
+        const bool poor = (double)hits * p.n > 4.0 * GVR_CAP * GUESS_NT;
+        uint32_t Ts;
+        if (poor) {
 #pragma unroll
-        for (int j = 0; j < SQ_N / GUESS_NT; ++j) {
-            const int q = c.tid + j * GUESS_NT;
-            sq[q] = f2key(ld_gather(p.x + (int)(((int64_t)q * p.n) / SQ_N)));
+            for (int j = 0; j < SQ_N / GUESS_NT; ++j) {
+                const int q = c.tid + j * GUESS_NT;
+                sq[q] = f2key(ld_gather(p.x + (int)(((int64_t)q * p.n) / SQ_N)));
+            }
+            const int rank = (int)ceil((2.5 * k + 512.0) * SQ_N / p.n);
+            Ts = sample_rank_key<SQ_N>(c, sq, sh, rank < SQ_N ? rank : SQ_N);
+        } else {
+            sq[c.tid] = f2key(xs);
+            const int rank = (int)ceil(4.0 * k * GUESS_NT / p.n);
+            Ts = sample_rank_key<GUESS_NT>(c, sq, sh, rank < GUESS_NT ? rank : GUESS_NT);
         }
-        const int rank = (int)ceil((2.5 * k + 512.0) * SQ_N / p.n);
-        const uint32_t Ts = sample_rank_key(c, sq, sh, rank < SQ_N ? rank : SQ_N);
         if (Ts > g.Tc) {
             g.Tc = Ts;
             g.tmin = 0u;
