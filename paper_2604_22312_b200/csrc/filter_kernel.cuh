@@ -41,27 +41,36 @@ static_assert(F_CTAS_PER_SM * (F_SMEM_BYTES + 1024) <= 233472, "three filter CTA
 // stage phases stay in step).  Virtual tiles past a row's real tiles are skipped.
 struct RoundIter {
     long long v, ve;
-    int r = -1;
+    int r, t;            // row and tile of virtual position v (tracked incrementally)
+    int loaded = -1;     // row whose plan p holds
     RowPlan p;
     int t0 = 0, nt = 0;
     bool last = false;  // last round of this CTA's segment of row r
+    __device__ __forceinline__ void start(long long vb, long long vend, int tpr)
+    {
+        v = vb;
+        ve = vend;
+        r = (int)(vb / tpr);
+        t = (int)(vb - (long long)r * tpr);
+    }
     __device__ __forceinline__ bool next(const float* scores, int64_t stride, const int32_t* row_lens, int k, int tpr)
     {
         while (v < ve) {
-            const int rr = (int)(v / tpr);
-            const int t = (int)(v - (long long)rr * tpr);
-            if (rr != r) {
-                r = rr;
-                p = plan_row(scores, stride, row_lens, rr, k);
+            if (loaded != r) {
+                loaded = r;
+                p = plan_row(scores, stride, row_lens, r, k);
             }
-            if (t >= p.ntiles) {
-                v = (long long)(rr + 1) * tpr;
+            if (t >= p.ntiles) {  // past the row's real tiles: on to the next row
+                v += tpr - t;
+                ++r;
+                t = 0;
                 continue;
             }
             t0 = t;
             nt = (int)min((long long)min(ROUND_STAGES, p.ntiles - t), ve - v);
             v += nt;
-            last = t0 + nt >= p.ntiles || v >= ve;
+            t += nt;
+            last = t >= p.ntiles || v >= ve;
             return true;
         }
         return false;
@@ -113,8 +122,7 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     const int b = blockIdx.x;
     const long long vb = cl_begin(cl, b), ve = cl_begin(cl, b + 1);
     RoundIter prod;  // thread 0: two rounds ahead of the consumers
-    prod.v = vb;
-    prod.ve = ve;
+    prod.start(vb, ve, cl.tpr);
     int issued = 0;
     if (c.tid == 0) {
         for (int s = 0; s < F_NSTAGE; ++s) mbar_init(ring.full(s), 1);
@@ -132,17 +140,21 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     const int regcap = cl.reg;
     const uint64_t keep = policy_evict_last();
     RoundIter it;
-    it.v = vb;
-    it.ve = ve;
+    it.start(vb, ve, cl.tpr);
     const int lb = lane_base(c.warp, c.lane);
     int cur_r = -1, seg_start = 0;
     float Tf = 0.f;
+    // T_c of the row after the current one, loaded a whole segment ahead of its use
+    const int r_first = it.r;
+    uint32_t tc_next = r_first < cl.V / cl.tpr ? __ldcg(&gp[r_first].Tc) : 0u;
     uint32_t kmax = 0u;  // this thread's largest candidate key in the current segment
     for (int i = 0; it.next(scores, stride, row_lens, k, cl.tpr); ++i) {
         const RowPlan& p = it.p;
         if (it.r != cur_r) {
+            const uint32_t tc = it.r == (cur_r < 0 ? r_first : cur_r + 1) ? tc_next : __ldcg(&gp[it.r].Tc);
             cur_r = it.r;
-            Tf = key2f(gp[cur_r].Tc);
+            Tf = key2f(tc);
+            if (cur_r + 1 < cl.V / cl.tpr) tc_next = __ldcg(&gp[cur_r + 1].Tc);
         }
         // unaligned head scalars (round holding tile 0) and tail scalars (round holding the
         // last tile), loaded before the wait so their latency hides behind it
@@ -203,7 +215,6 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             const uint32_t wk = __reduce_max_sync(FULL, kmax);
             if (c.lane == 0 && wk) atomicMax(seg_kmax, wk);
             kmax = 0u;
-            __threadfence();
         }
         c.sync();  // the round's stages are consumed and its reservations made
         if (c.tid == 0 && prod.next(scores, stride, row_lens, k, cl.tpr)) issue_pair(ring, prod, i + F_ROUNDS);
@@ -219,6 +230,9 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 seg_start = end;
                 if (bq.queue) {
                     const int ns = cl_cta_of(cl, v0 + p.ntiles - 1) - b0 + 1;
+                    // the round barrier ordered every thread's candidate stores before this
+                    // point; the fence makes them (and the record) visible device-wide
+                    // before the count (the grid-barrier release pattern)
                     __threadfence();
                     if (atomicAdd(bq.segdone + cur_r, 1) == ns - 1) {
                         __threadfence();  // the other segments' records and entries happen-before the push
