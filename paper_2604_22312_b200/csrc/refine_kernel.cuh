@@ -45,51 +45,34 @@ __device__ __forceinline__ int h16_add(uint32_t* w, int b)
     return (int)((atomicAdd(&w[b >> 1], 1u << sh) >> sh) & 0xffffu);
 }
 
-// Entries q0, q0 + stride, ... of the row's list (segment s: entries [cum[s], cum[s+1]) at
-// region[gs[s] + q - cum[s]], read through L2), or of the row itself when rowx != nullptr.
-// Keys only (the histogram passes): entries q0, q0 + stride, ... as list_load.
-template <int UNR>
-__device__ __forceinline__ void list_keys(const CandLists& cl, const float* rowx, const int (&gs)[F_SEGS],
-                                          const int (&cum)[F_SEGS + 1], int total, int q0, int stride, uint32_t (&kv)[UNR])
+// Visit the row's list in batches of UNR entries per thread, segment by segment (segment s:
+// n[s] entries from region position gs[s]; a row with len <= k is one segment read from
+// the row itself, rowx).  fn(kv, pos, valid) gets the keys, the entries' region positions
+// (or row positions) and a validity mask.
+template <int UNR, class Fn>
+__device__ __forceinline__ void for_list(const RefineGroup& c, const CandLists& cl, const float* rowx,
+                                         const int (&gs)[F_SEGS], const int (&n)[F_SEGS], Fn&& fn)
 {
     const uint32_t* rk = reinterpret_cast<const uint32_t*>(cl.region);
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        const int q = q0 + u * stride;
-        if (rowx) {
-            kv[u] = q < total ? f2key(__ldg(rowx + q)) : 0u;
-            continue;
+    for (int s = 0; s < F_SEGS; ++s) {
+        const int base = gs[s], ns = n[s];
+        for (int j0 = c.tid; j0 < ns; j0 += UNR * RF_NT) {
+            uint32_t kv[UNR];
+            int pos[UNR];
+            uint32_t valid = 0u;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int j = j0 + u * RF_NT;
+                pos[u] = base + j;
+                kv[u] = 0u;
+                if (j < ns) {
+                    kv[u] = rowx ? f2key(__ldg(rowx + pos[u])) : __ldcg(rk + 2 * (size_t)pos[u]);
+                    valid |= 1u << u;
+                }
+            }
+            fn(kv, pos, valid);
         }
-        int s = 0;
-#pragma unroll
-        for (int v = 1; v < F_SEGS; ++v) s += q >= cum[v];
-        const int base = s == 0 ? gs[0] : s == 1 ? gs[1] : s == 2 ? gs[2] : gs[3];
-        const int c0 = s == 0 ? cum[0] : s == 1 ? cum[1] : s == 2 ? cum[2] : cum[3];
-        kv[u] = q < total ? __ldcg(rk + 2 * (size_t)(base + (q - c0))) : 0u;
-    }
-}
-
-template <int UNR>
-__device__ __forceinline__ void list_load(const CandLists& cl, const float* rowx, const int (&gs)[F_SEGS],
-                                          const int (&cum)[F_SEGS + 1], int total, int q0, int stride, uint2 (&e)[UNR])
-{
-    if (rowx) {  // a row with len <= k is its own list: (key, position)
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const int q = q0 + u * stride;
-            e[u] = q < total ? make_uint2(f2key(__ldg(rowx + q)), (uint32_t)q) : make_uint2(0u, 0u);
-        }
-        return;
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        const int q = q0 + u * stride;
-        int s = 0;
-#pragma unroll
-        for (int v = 1; v < F_SEGS; ++v) s += q >= cum[v];
-        const int base = s == 0 ? gs[0] : s == 1 ? gs[1] : s == 2 ? gs[2] : gs[3];
-        const int c0 = s == 0 ? cum[0] : s == 1 ? cum[1] : s == 2 ? cum[2] : cum[3];
-        e[u] = q < total ? __ldcg(cl.region + base + (q - c0)) : make_uint2(0u, 0u);
     }
 }
 
@@ -111,9 +94,13 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     const int K = k;
     constexpr int BPT = NBINS / RF_NT;
     constexpr int UNR = 8;
+    // thread 0 claims the next queue slot during the current row's last step (ranking),
+    // so the claim's round trip is off the critical path without hoarding rows early
+    int next_slot = -1;
     for (;;) {
         if (c.tid == 0) {
-            const int slot = atomicAdd(bq.qctl + Q_HEAD, 1);
+            const int slot = next_slot >= 0 ? next_slot : atomicAdd(bq.qctl + Q_HEAD, 1);
+            next_slot = -1;
             int r = -1;
             if (slot < num_rows) {
                 int v;
@@ -163,15 +150,16 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             }
         }
         c.sync();
-        int gs[F_SEGS], cum[F_SEGS + 1];
+        int gs[F_SEGS], ns[F_SEGS];
+#pragma unroll
+        for (int s = 0; s < F_SEGS; ++s) gs[s] = ns[s] = 0;
         if (p.ntiles > 0) {
             total = c.misc[22];
             kmax = (uint32_t)c.misc[23];
-            cum[0] = 0;
 #pragma unroll
             for (int s = 0; s < F_SEGS; ++s) {
                 gs[s] = c.misc[24 + 2 * s];
-                cum[s + 1] = cum[s] + c.misc[25 + 2 * s];
+                ns[s] = c.misc[25 + 2 * s];
             }
         }
         bool ok = p.ntiles > 0 && p.n > k && total >= K && total <= RF_MAXLIST && kmax >= Tc;
@@ -191,6 +179,10 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             rowx = p.x;
             total = p.n;
             take = p.n;
+            gs[0] = 0;  // one segment: the row itself
+            ns[0] = p.n;
+#pragma unroll
+            for (int s = 1; s < F_SEGS; ++s) ns[s] = 0;
             Tc = mn;
             kmax = mx2;
             ok = p.n > 0;
@@ -214,17 +206,14 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 c.sync();
                 scale = bin_scale((uint64_t)kmax - lo + 1ull);
                 uint32_t f = 0;
-                constexpr int UK = 16;
-                for (int q0 = c.tid; q0 < total; q0 += UK * RF_NT) {
-                    uint32_t kv[UK];
-                    list_keys<UK>(cl, rowx, gs, cum, total, q0, RF_NT, kv);
+                for_list<16>(c, cl, rowx, gs, ns, [&](const uint32_t (&kv)[16], const int (&)[16], uint32_t valid) {
 #pragma unroll
-                    for (int u = 0; u < UK; ++u)
-                        if (q0 + u * RF_NT < total && kv[u] >= lo) {
+                    for (int u = 0; u < 16; ++u)
+                        if ((valid >> u & 1u) && kv[u] >= lo) {
                             h16_add(hist, (NBINS - 1) - lin_bin(kv[u] - lo, scale));
                             ++f;
                         }
-                }
+                });
                 f = group_red1<R_ADD>(c, f);  // its barrier also completes the histogram
                 if (lvl == 0) {
                     ftc = (int)f;
@@ -279,18 +268,20 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 }
                 c.sync();
                 // ---- counting sort of the bins up to the K-th bin (composites)
-                for (int q0 = c.tid; q0 < total; q0 += UNR * RF_NT) {
-                    uint2 e[UNR];
-                    list_load<UNR>(cl, rowx, gs, cum, total, q0, RF_NT, e);
+                for_list<UNR>(c, cl, rowx, gs, ns, [&](const uint32_t (&kv)[UNR], const int (&pos)[UNR], uint32_t valid) {
+                    int b[UNR], ix[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        b[u] = (valid >> u & 1u) && kv[u] >= lo ? (NBINS - 1) - lin_bin(kv[u] - lo, scale) : NBINS;
+                        ix[u] = b[u] <= bk ? (rowx ? pos[u] : __ldcg(cl.region + pos[u]).y) : 0;
+                    }
 #pragma unroll
                     for (int u = 0; u < UNR; ++u)
-                        if (q0 + u * RF_NT < total && e[u].x >= lo) {
-                            const int b = (NBINS - 1) - lin_bin(e[u].x - lo, scale);
-                            if (b <= bk) cs[h16_add(cur, b)] = make_comp(e[u].x, (int32_t)e[u].y);
-                        }
-                }
+                        if (b[u] <= bk) cs[h16_add(cur, b[u])] = make_comp(kv[u], ix[u]);
+                });
                 c.sync();
                 if (phase_ts) tsr[TS_PHASE4] = clock64();
+                if (c.tid == 0) next_slot = atomicAdd(bq.qctl + Q_HEAD, 1);
                 // ---- rank inside the bin; positions < K are the ordered output
                 int32_t* o = out + (int64_t)r * k;
                 float* ov = out_val ? out_val + (int64_t)r * k : nullptr;

@@ -589,3 +589,23 @@ def test_filter_and_row_paths_agree_on_cfg4(gvr):
                        options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
         torch.cuda.synchronize()
         _assert_rows(out.cpu().numpy(), ref, lens)
+
+
+def test_filter_path_alternating_batch_sizes_and_paths(gvr):
+    """The per-stream scratch (ready queue, control words, candidate regions) is reused
+    across calls of different batch sizes, row lengths and batch paths: every call is
+    exact.  (Its zero words live at fixed offsets sized by the lease's row capacity.)"""
+    import torch
+    dev = torch.device("cuda:0")
+    jobs = [(320, 12_000, 0), (488, 20_000, 0), (300, 9_000, 0), (330, 16_000, 1), (420, 7_000, 0),
+            (300, 12_000, 0)]
+    for i, (R, n, path) in enumerate(jobs):
+        rng = np.random.default_rng(1500 + i)
+        host = rng.standard_normal((R, n)).astype(np.float32)
+        lens = rng.integers(n // 2, n + 1, size=R).astype(np.int32)
+        # a correlated previous step: the Top-K of a noisy copy of each row
+        prev = oracle.topk_batched(host + 0.3 * rng.standard_normal((R, n)).astype(np.float32), K, row_lens=lens)
+        out = gvr.topk(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
+                       prev=torch.from_numpy(prev).to(dev), options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
+        torch.cuda.synchronize()
+        _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens)
