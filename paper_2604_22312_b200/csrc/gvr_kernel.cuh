@@ -627,11 +627,14 @@ __device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const i
     float gv[GPT];
     uint32_t valid = 0;
     if (pr) {
+        // the guessed positions used are q = m * stride, m < ceil(k / stride), spread
+        // evenly over the threads (m = tid + j * N): no per-slot modulo, no idle threads
+        const int M = (k + stride - 1) / stride;
         int32_t gi[GPT];
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
-            const int q = c.tid + j * G::N;
-            gi[j] = (q < k && q % stride == 0) ? __ldg(pr + q) : -1;
+            const int m = c.tid + j * G::N;
+            gi[j] = m < M ? __ldg(pr + m * stride) : -1;
         }
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
@@ -765,7 +768,7 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     // the ready queue now (the refine kernel hands it on to the fixup list)
     if (bq.queue && p.ntiles == 0 && c.tid == 0) st_release(bq.queue + atomicAdd(bq.qctl + Q_TAIL, 1), r + 1);
     if (p.n <= k) {  // trivial row: no guess needed (block-uniform); scheduled last
-        if (c.tid == 0) sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
+        if (c.tid == 0 && !bq.queue) sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
         return;
     }
     // one strided row sample per thread, gathered alongside the guess values
@@ -807,10 +810,12 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     }
     if (c.tid == 0) {
         gp[r] = g;
-        if (heavy)
-            sched.order[atomicAdd(sched.cursors, 1)] = r;
-        else
-            sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
+        if (!bq.queue) {  // the row path's order: heavy rows first (the filter path needs none)
+            if (heavy)
+                sched.order[atomicAdd(sched.cursors, 1)] = r;
+            else
+                sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
+        }
     }
 }
 
