@@ -431,8 +431,9 @@ def main():
         if fused:
             stream_kernel, n_kernels, gvr_path = "gvr_topk_kernel", 1, "fused single kernel (one wave)"
         elif args.path == "filter":
-            stream_kernel, n_kernels = "gvr_filter_kernel", 3
-            gvr_path = "guess kernel + filter kernel (whole batch, one HBM pass) + refine kernel (one CTA per row)"
+            stream_kernel, n_kernels = "gvr_filter_kernel", 4  # guess, filter, refine, fixup
+            gvr_path = ("guess kernel + filter kernel (whole batch, one HBM pass) + refine kernel (rows from their "
+                        "candidate lists) + fixup kernel (rows the lists cannot finish; usually none)")
         else:
             stream_kernel, n_kernels, gvr_path = "gvr_topk_kernel", 2, "guess kernel + row streaming kernel"
 
