@@ -15,9 +15,13 @@
  *   same bytes for the same input; the guess never changes the result.
  *
  * Conventions shared by every entry point:
- *   - Device pointers are caller-owned CUDA device pointers.  The library allocates
- *     nothing per call and keeps no reference after return (CUDA-Graph capturable;
- *     the stable-address requirement of PAPER.md:1476-1482).
+ *   - Device pointers are caller-owned CUDA device pointers; the library keeps no
+ *     reference to them after return.  Its only memory is a scratch lease per (device,
+ *     stream) — Phase-1 hand-off, ready queue and, on the batch filter path, candidate
+ *     lists (8 B per entry, room for 1/8 of the batch's elements; ~60 MB for 488 rows
+ *     of 100K) — grown stream-ordered from a private pool on first use and reused, so
+ *     steady-state calls allocate nothing (CUDA-Graph capturable; the stable-address
+ *     requirement of PAPER.md:1476-1482).
  *   - Calls are stream-ordered on `stream` (0 = legacy default stream) and do not
  *     synchronise the host, except gvr_topk_batched_host (documented below).
  *   - Layout: scores is row-major [num_rows, row_stride] fp32; row r occupies
