@@ -76,7 +76,8 @@ typedef struct {
     int32_t cand_count;     /* candidates collected in Phase 3 (|{x >= T}|)           */
     int32_t done_kind;      /* gvr_done_kind                                          */
     int32_t global_passes;  /* full-row reads of the row from global memory           */
-    int32_t raises;         /* mid-stream collect-threshold raises         */
+    int32_t raises;         /* row kernel: mid-stream collect-threshold raises; filter */
+                            /* path refine: Phase-4 histogram narrowings  */
     int32_t buffer_count;   /* f(T_c): size of the streamed candidate buffer          */
     int32_t cluster;        /* CTAs cooperating on the row                            */
 } gvr_row_stats;

@@ -188,7 +188,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             ok = p.n > 0;
         }
         if (phase_ts) tsr[TS_PHASE1] = clock64();
-        int ftc = 0, nsel = 0;
+        int ftc = 0, nsel = 0, levels = 0;
         if (ok) {
             // ---- Phase 4: histogram of the keys >= lo over [lo, kmax],
             // the K-th bin from the bin scan.  lo starts at T_c; if the
@@ -201,6 +201,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             int h[BPT];
             int bk = -1;
             for (int lvl = 0; lvl < 3; ++lvl) {
+                levels = lvl + 1;
                 for (int i = c.tid; i < NBINS / 2; i += RF_NT) hist[i] = 0u;
                 if (c.tid == 0) c.misc[12] = -1;  // K-th bin: set below by the thread that holds it
                 c.sync();
@@ -333,7 +334,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 s.cand_count = trivial ? p.n : ftc;
                 s.done_kind = trivial ? GVR_DONE_TRIVIAL : GVR_DONE_CONVERGED;
                 s.global_passes = 1;
-                s.raises = 0;
+                s.raises = levels > 1 ? levels - 1 : 0;  // Phase-4 histogram narrowings (R32)
                 s.buffer_count = trivial ? 0 : ftc;
                 s.cluster = 1;
                 stats[r] = s;
