@@ -56,10 +56,13 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 
 
 # ----------------------------------------------------------------------------- inputs
-def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0, first_layer=0):
+def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0, first_layer=0, rho=None):
     """Synthetic decode batch: rows (request, layer, draft j) of length n + j from the
     Eq. 1 indexer (synth.IndexerLayer), plus prev_topk = the exact Top-K of the
     request's previous step (n - 1 keys), shared by its draft rows.
+    Draft token j is one more AR(1) decode step of the query state than draft j - 1, so
+    the shared guess gets staler along the draft.  rho overrides the
+    per-layer AR coefficient (synth.layer_rho) for every layer.
     The previous step's Top-K is computed with the GVR kernel itself (no guess), i.e.
     the decode loop feeding its own output back; it is only a hint.
     `requests` is a count (requests 0..count-1) or an explicit list of global request
@@ -82,10 +85,12 @@ def make_decode_batch(requests, layers, n, dev, seed, draft=1, rank=0, first_lay
         for li in range(layers):
             l = first_layer + li
             s = synth.splitmix64(seed, rank, q, l)
-            lay = synth.IndexerLayer(S, synth.layer_rho(l, seed), s, dev)
+            lay = synth.IndexerLayer(S, synth.layer_rho(l, seed) if rho is None else rho, s, dev)
             prev_rows[qi * layers + li, :n - 1] = lay.scores(n - 1)
             lay.step()
             for j in range(draft):
+                if j:
+                    lay.step()
                 scores[row, :n + j] = lay.scores(n + j)
                 lens[row] = n + j
                 row += 1

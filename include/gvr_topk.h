@@ -68,10 +68,19 @@ typedef enum {
     GVR_DONE_RADIX = 3       /* radix-select entry point (baseline)                     */
 } gvr_done_kind;
 
+/* How Phase 2 ended (gvr_row_stats.phase2_exit; R34-R36). */
+typedef enum {
+    GVR_P2_ALL = 0,        /* len <= 6016: every element is collected, no search        */
+    GVR_P2_WINDOW = 1,     /* a probe's sample count fell in the window [L, H]          */
+    GVR_P2_TIES = 2,       /* the anchors became adjacent keys (ties): lo anchor taken  */
+    GVR_P2_EXHAUSTED = 3   /* 12 probes without a window hit: lo anchor taken           */
+} gvr_phase2_exit;
+
 /* Per-row statistics (optional output of the _ex entry point). Reported, not part of
  * the result contract. */
 typedef struct {
-    int32_t secant_iters;   /* I: threshold evaluations f(T) (Phase 2)  */
+    int32_t secant_iters;   /* I: threshold probes f(T) of Phase 2,  */
+                            /* counted over the row sample (R34)             */
     int32_t snap_iters;     /* S: Phase-4 snap iterations          */
     int32_t cand_count;     /* candidates collected in Phase 3 (|{x >= T}|)           */
     int32_t done_kind;      /* gvr_done_kind                                          */
@@ -80,12 +89,18 @@ typedef struct {
                             /* path refine: Phase-4 histogram narrowings  */
     int32_t buffer_count;   /* f(T_c): size of the streamed candidate buffer          */
     int32_t cluster;        /* CTAs cooperating on the row                            */
+    int32_t phase2_exit;    /* gvr_phase2_exit                                        */
+    int32_t sample_count;   /* sample hits at T_c (of 4096; R34)            */
+    uint32_t tc_key;        /* T_c as a sortable key               */
+    int32_t reserved;
 } gvr_row_stats;
 
 /* Tuning knobs; NULL selects the defaults.  None of them changes the result. */
 typedef struct {
-    float collect_sigma;      /* T_c = pmean - collect_sigma * sd(guess values); default 0.3 */
-    int32_t max_secant_iters; /* secant steps before pure bisection; default 8              */
+    float window_z;           /* Phase-2 window lower edge mu + z sqrt(mu) sample hits     */
+                              /* (R35); 0 or NaN = default 4.5; a negative z    */
+                              /* aims below the K-th value (forces the second pass, tests)*/
+    int32_t max_secant_iters; /* Phase-2 secant steps before pure bisection; default 8     */
     int32_t force_cluster;    /* 0 = automatic; else CTAs per row (1,2,4,8)                */
     int32_t guess_stride;     /* Phase-1 statistics over every n-th guessed position;      */
                               /* 0 = default 4 (R29); 1 = all of them, as in    */

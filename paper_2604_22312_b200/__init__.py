@@ -27,13 +27,14 @@ LIB_PATH = os.path.join(_HERE, "libgvrtopk.so")
 _lib = None
 
 STATS_FIELDS = ("secant_iters", "snap_iters", "cand_count", "done_kind", "global_passes",
-                "raises", "buffer_count", "cluster")
+                "raises", "buffer_count", "cluster", "phase2_exit", "sample_count", "tc_key", "reserved")
+PHASE2_EXITS = {0: "all", 1: "window", 2: "ties", 3: "exhausted"}
 DONE_KINDS = {0: "trivial", 1: "converged", 2: "tiefill", 3: "radix"}
 MAX_K = 2048
 
 
 class GvrOptions(ctypes.Structure):
-    _fields_ = [("collect_sigma", ctypes.c_float), ("max_secant_iters", ctypes.c_int32),
+    _fields_ = [("window_z", ctypes.c_float), ("max_secant_iters", ctypes.c_int32),
                 ("force_cluster", ctypes.c_int32), ("guess_stride", ctypes.c_int32),
                 ("batch_path", ctypes.c_int32)]
 
@@ -151,7 +152,8 @@ def topk(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, stream=None
 
 def topk_ex(scores, k: int = MAX_K, row_lens=None, prev=None, out=None, values: bool = True,
             stats: bool = True, options: GvrOptions | None = None, stream=None):
-    """GVR Top-K plus optional selected values [R, k] and per-row stats [R, 8] (int32)."""
+    """GVR Top-K plus optional selected values [R, k] and per-row stats [R, 12] (int32,
+    columns STATS_FIELDS; tc_key is the uint32 bit pattern)."""
     torch = _torch()
     R, stride, row_lens, prev, out = _prep(scores, k, row_lens, prev, out)
     val = torch.empty((R, k), dtype=torch.float32, device=scores.device) if values else None

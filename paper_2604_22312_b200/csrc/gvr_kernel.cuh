@@ -5,18 +5,22 @@
 //
 // Method: PAPER.md Sec. 4 (lines 379-690).  Per row:
 //   Phase 1 (Guess): x at the previous step's Top-K positions ->
-//     pmin / pmax / pmean (Eq. 4) plus the second moment; T_c = pmean - sigma*sd.  Runs
-//     as a separate short kernel (gvr_guess_kernel) ahead of the streaming kernel.
-//   Streaming pass (B200 re-design of the Phase-2 count pass fused with the Phase-3
-//     collector): the row body is read from HBM exactly once, in
-//     rounds of 2 x 16 KB TMA tiles; every element whose key is >= T_c is appended to
-//     B (warp scan + one shared atomic per warp: ballot-free).
-//     B holds {x >= T_c}, so f(T) for every T >= T_c is counted from B alone (Lemma 1,
-//     PAPER.md:401-415).  If B would overflow, T_c is raised by a secant search over B
-//     (Eq. 6) to a threshold that still keeps >= K elements.
-//   Phase 2: secant search of Eq. 6 toward f_target inside the
-//     window K <= f(T) <= C, starting from T0 = pmean, with first-step damping and
-//     bisection fallback — counts from B (shared memory), not from HBM.
+//     pmin / pmax / pmean (Eq. 4).
+//   Phase 2: the secant search of Eq. 6 for a collect threshold T_c
+//     whose count lies in a target window — T0 = pmean first, then the Phase-1 bracket
+//     end on the far side, then Eq.-6 steps (first one damped <= 0.5, key-space bisection
+//     at float precision limits).  Each count f(T) is taken over a fixed 4096-value row
+//     sample held in registers (16 contiguous floats per thread), not over the row in
+//     HBM: the window is the sample image of [K, C] with a margin that keeps
+//     f(T_c) >= K (R34-R36).  Phases 1-2 run in gvr_guess_kernel on the batch
+//     paths and inside the row's CTA on the fused / cluster paths (phase12()).
+//   Streaming pass (B200 re-design of the Phase-3 collector): the row
+//     body is read from HBM exactly once, in rounds of 2 x 16 KB TMA tiles; every element
+//     whose key is >= T_c is appended to B (warp scan + one shared atomic per warp:
+//     ballot-free).  B holds {x >= T_c}, so f(T) for every T >= T_c is
+//     counted from B alone (Lemma 1).  If B would overflow, T_c is
+//     raised by a key-space histogram search over B (R23) to a threshold that still keeps
+//     >= K elements.
 //   Phase 3: ballot-free compaction of B to {x >= T} reusing the
 //     per-thread counts of the last count pass (count cache).
 //   Phase 4: 2048-bin histogram over the candidate key range,
@@ -26,8 +30,8 @@
 //     all candidates); exact narrowing of the bin if it is too large.
 //   Ordered output: candidates >= T* sorted by (key desc, index asc), first K written.
 //   Fallbacks (R12/R13): massive ties or an
-//     overshooting guess (f(T_c) < K) -> exact radix select + ordered tie fill from
-//     global memory.
+//     overshooting threshold (f(T_c) < K) -> a second stream at a lower threshold, exact
+//     radix select + ordered tie fill from global memory.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -37,8 +41,8 @@
 namespace gvr {
 
 struct GvrParams {
-    float collect_sigma;
-    int max_secant;
+    float window_z;  // Phase-2 window lower edge: mu + z sqrt(mu) sample hits (R35)
+    int max_secant;  // secant steps before pure bisection (R11)
     int guess_stride;  // Phase-1 statistics over every guess_stride-th guessed position (R29)
 };
 
@@ -81,14 +85,20 @@ __device__ __forceinline__ long long sm_id()
     return (long long)s;
 }
 
-// What Phase 1 (gvr_guess_kernel) hands to the streaming kernel, per row.
+// What Phases 1-2 (phase12) hand to the streaming step, per row (32 bytes).
 struct GuessOut {
-    uint32_t Tc;    // collect threshold key
-    uint32_t T0;    // f2key(pmean), the Phase-2 start
-    int32_t t0_ok;  // pmean finite
-    uint32_t tmin;  // second-pass threshold: pmin when all k guesses were gathered and
-                    // valid (then f(pmin) >= k for distinct guesses), else 0 (everything)
+    uint32_t Tc;     // collect threshold key (Phase 2 result)
+    uint32_t T0;     // f2key(pmean), the Phase-2 start
+    uint32_t tmin;   // second-pass threshold: pmin when all k guesses were gathered and
+                     // valid (then f(pmin) >= k for distinct guesses), else 0 (everything)
+    uint32_t top;    // max(pmax, sample max) key
+    int32_t t0_ok;   // pmean finite
+    int16_t iters;   // Phase-2 probes I
+    int16_t exit;    // gvr_phase2_exit
+    int32_t scount;  // sample hits at T_c
+    int32_t pad;
 };
+static_assert(sizeof(GuessOut) == 32, "GuessOut layout");
 
 // Batch path (filter_kernel.cuh): where gvr_filter_kernel left each row's candidates.
 constexpr int F_SEGS = 4;  // most filter CTAs covering one row (host-enforced)
@@ -146,8 +156,6 @@ struct RowMeta {
     uint32_t ftc;     // f(T_c) = fill - extras
     uint32_t kmax;    // max key in B
     uint32_t extras;  // superset entries (NaN / -0 against +0) with key < T_c
-    uint32_t T0;      // f2key(pmean)
-    bool t0_ok;
 };
 
 // Secant step of Eq. 6 in value space between the anchors
@@ -415,61 +423,21 @@ __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const R
     return rc;
 }
 
-// Phases 2-4 and the ordered output of one streamed row.
-// st = {secant_iters, snap_iters, cand_count, needs_tiefill}.
+// Phases 3-4 and the ordered output of one streamed row (Phase 2 ran before the stream,
+// phase12): B holds f(T_c) <= capacity entries, so no further threshold search is needed.
+// st = {unused, snap_iters, cand_count, needs_tiefill}.
 __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work& Wk, const RowMeta& meta,
-                                           const GvrParams& prm, int k, int32_t* o, float* ov, int (&st)[4],
-                                           long long* ts)
+                                           int k, int32_t* o, float* ov, int (&st)[4], long long* ts)
 {
     const int K = k;
     const int fill = meta.fill;
-    const uint32_t Tc = meta.Tc;
-    const uint32_t ftc = meta.ftc;
     const uint32_t kmax = meta.kmax;
     const uint32_t extras = meta.extras;
-    const uint32_t T0 = meta.T0;
-    const bool t0_ok = meta.t0_ok;
-    st[0] = 1;  // f(T_c) was counted during the stream
-    // ---------------- Phase 2: secant search over B
-    uint32_t T = Tc;
+    const uint32_t T = meta.Tc;
     ChunkCounts cc;
-    if (ftc > (uint32_t)CWIN) {
-        uint64_t lo = Tc, hi = (uint64_t)kmax + 1ull;  // kmax = max key in B
-        uint32_t clo = ftc, chi = 0;
-        const float target = 0.5f * (float)(K + CWIN);  // f_target
-        bool have_t0 = t0_ok && (uint64_t)T0 > lo && (uint64_t)T0 < hi;
-        bool first_secant = true;
-        for (int it = 0;; ++it) {
-            if (hi - lo < 2 || it >= 64) {
-                T = (uint32_t)lo;  // f(lo) <= cap: B itself is a valid candidate set
-                cc = count_chunks_ge(c, B, fill, T);
-                break;
-            }
-            if (have_t0) {
-                T = T0;  // Phase 2 starts at T0 = pmean
-                have_t0 = false;
-            } else {
-                T = secant_step(lo, clo, hi, chi, target, first_secant, it >= prm.max_secant);
-                first_secant = false;
-            }
-            cc = count_chunks_ge(c, B, fill, T);
-            const uint32_t f = group_red1<R_ADD>(c, chunk_total(cc));
-            ++st[0];
-            if (f >= (uint32_t)K && f <= (uint32_t)CWIN) break;
-            if (f > (uint32_t)CWIN) {
-                lo = T;
-                clo = f;
-            } else {
-                hi = T;
-                chi = f;
-            }
-        }
-    }
     // ---------------- Phase 3: ballot-free compaction
     int cand = fill;
-    if (T != Tc) {
-        cand = compact_ge(c, B, fill, T, cc);
-    } else if (extras != 0u) {
+    if (extras != 0u) {
         cc = count_chunks_ge(c, B, fill, T);
         cand = compact_ge(c, B, fill, T, cc);
     }
@@ -615,20 +583,78 @@ __device__ __forceinline__ float ld_gather(const float* p)
     asm volatile("ld.global.nc.L1::no_allocate.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return v;
 }
-
-// Phase 1 (Eq. 4) for one row by group c: gathers the guessed values,
-// reduces pmin / pmax / pmean and the second moment, and returns T_c, T0 (R22, R7).
-template <class G>
-__device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm)
+// Row-sample chunk load (Phase 2): 16 contiguous bytes of a 64-byte chunk, no L1 allocation.
+__device__ __forceinline__ float4 ldg_sample(const float4* p)
 {
-    constexpr int GPT = KMAX / G::N;  // 8 guesses per thread
-    // subsampled statistics only for long rows (K/N <= 1/32, R29)
-    const int stride = p.n >= 32 * k ? prm.guess_stride : 1;
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Deterministic fp32 sum of one channel over the group: fixed xor-shuffle tree per warp,
+// then the same tree over the warp sums (lanes >= W contribute 0) — the order the CPU
+// replay (oracle/phase2_replay.py) follows.
+template <class G>
+__device__ __forceinline__ float group_fsum1(G& c, float a)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = __fadd_rn(a, __shfl_xor_sync(FULL, a, o));
+    float* s = c.redf + c.par * 2 * G::W;
+    if (c.lane == 0) s[c.warp] = a;
+    c.sync();
+    a = c.lane < G::W ? s[c.lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = __fadd_rn(a, __shfl_xor_sync(FULL, a, o));
+    c.par ^= 1;
+    return a;
+}
+
+// Phase-2 constants (R34-R36).
+constexpr int P2_CHUNK = 16;                 // floats per sample chunk (one 64-byte read)
+constexpr int P2_S = 256 * P2_CHUNK;         // sample values: one chunk per thread
+constexpr int P2_MAX_ITERS = 12;             // probes before the Phase-2 fallback (R12)
+constexpr float P2_Z_DEFAULT = 4.5f;
+
+// Phases 1-2 for one row by a 256-thread group (R7, R8-R12,
+// R19, R29, R34-R36).  Every fp32 operation is explicit round-to-nearest in a fixed
+// order, so the CPU replay reproduces T_c, I and the exit kind bit for bit.
+//   Phase 1: the guessed values x[q], q = prev[m * stride] for m < ceil(k / stride)
+//     (thread t holds m = t + 256 j) -> pmin / pmax (keys), pmean = sum / count (Eq. 4).
+//     No valid guess -> the statistics of the row sample.
+//   Sample: chunk t (16 contiguous floats of the 16-byte aligned body, chunk start
+//     16 * floor(t * nch / 256) of nch = body / 16 chunks) in registers, as keys.
+//   Phase 2: window [L, H] in sample hits, L = ceil(mu + z sqrt(mu)) with mu = k S / n
+//     the expected hits at the K-th value, H = L + ceil(L / 2), target (L + H) / 2;
+//     anchors exact for the sample: (min key, S), (max key + 1, 0) (R8).  Probe T0 =
+//     pmean, then the bracket end pmin (f(T0) below the window) or
+//     pmax (above), then Eq. 6 steps (secant_step) — a probe with L <= hits <= H ends
+//     the search.  Adjacent anchors (ties) or P2_MAX_ITERS probes -> the lo anchor, whose
+//     hits are above the window.
+template <class G>
+__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm)
+{
+    static_assert(G::N == 256, "one sample chunk per thread");
+    constexpr int GPT = KMAX / G::N;  // 8 guessed positions per thread
+    GuessOut g;
+    g.pad = 0;
+    if (p.n <= GVR_CAP) {  // the whole row fits in B: collect everything, no search
+        g.Tc = 0u;
+        g.T0 = 0u;
+        g.tmin = 0u;
+        g.top = 0xffffffffu;
+        g.t0_ok = 0;
+        g.iters = 0;
+        g.exit = GVR_P2_ALL;
+        g.scount = 0;
+        return g;
+    }
+    // ---- loads: the guessed values (two dependent round trips) and the sample chunk
+    const int stride = p.n >= 32 * k ? prm.guess_stride : 1;  // R29
     float gv[GPT];
     uint32_t valid = 0;
     if (pr) {
-        // the guessed positions used are q = m * stride, m < ceil(k / stride), spread
-        // evenly over the threads (m = tid + j * N): no per-slot modulo, no idle threads
         const int M = (k + stride - 1) / stride;
         int32_t gi[GPT];
 #pragma unroll
@@ -644,9 +670,33 @@ __device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const i
                 valid |= 1u << j;
             }
         }
+    } else {
+#pragma unroll
+        for (int j = 0; j < GPT; ++j) gv[j] = 0.f;
     }
-    uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u, unused = 0u;
-    float sum = 0.f, sq = 0.f;
+    const int nch = p.nfl / P2_CHUNK;  // >= 376 for n > GVR_CAP
+    const float4* sp4 =
+        reinterpret_cast<const float4*>(p.x + p.head + P2_CHUNK * (int)(((int64_t)c.tid * nch) >> 8));
+    float sv[P2_CHUNK];
+#pragma unroll
+    for (int q = 0; q < P2_CHUNK / 4; ++q) {
+        const float4 v = ldg_sample(sp4 + q);
+        sv[4 * q] = v.x;
+        sv[4 * q + 1] = v.y;
+        sv[4 * q + 2] = v.z;
+        sv[4 * q + 3] = v.w;
+    }
+    uint32_t sk[P2_CHUNK];
+    uint32_t smin = 0xffffffffu, smax = 0u;
+#pragma unroll
+    for (int q = 0; q < P2_CHUNK; ++q) {
+        sk[q] = f2key(sv[q]);
+        smin = min(smin, sk[q]);
+        smax = max(smax, sk[q]);
+    }
+    // ---- Phase 1 (Eq. 4)
+    uint32_t kmn = 0xffffffffu, kmx = 0u, cnt = 0u;
+    float sum = 0.f;
 #pragma unroll
     for (int j = 0; j < GPT; ++j) {
         if ((valid >> j) & 1u) {
@@ -654,100 +704,106 @@ __device__ __forceinline__ GuessOut phase1_guess(G& c, const RowPlan& p, const i
             kmn = min(kmn, kv);
             kmx = max(kmx, kv);
             ++cnt;
-            sum += gv[j];
-            sq += gv[j] * gv[j];
+        }
+        sum = __fadd_rn(sum, gv[j]);  // invalid slots add +0
+    }
+    group_red4<R_MIN, R_MAX, R_ADD, R_MAX>(c, kmn, kmx, cnt, smax);
+    smin = group_red1<R_MIN>(c, smin);
+    bool complete = cnt == (uint32_t)k && stride == 1;
+    if (cnt == 0) {  // no valid guess: statistics of the row sample (R7)
+        sum = 0.f;
+#pragma unroll
+        for (int q = 0; q < P2_CHUNK; ++q) sum = __fadd_rn(sum, sv[q]);
+        kmn = smin;
+        kmx = smax;
+        cnt = P2_S;
+        complete = false;
+    }
+    sum = group_fsum1(c, sum);
+    const float pmean = __fdiv_rn(sum, (float)cnt);
+    // ---- Phase 2 over the sample (Eq. 6)
+    const float mu = __fdiv_rn((float)(k * P2_S), (float)p.n);
+    const int L = min(max((int)ceilf(__fadd_rn(mu, __fmul_rn(prm.window_z, __fsqrt_rn(mu)))), 1), P2_S);
+    const int H = min(L + (L + 1) / 2, P2_S);
+    const float ft = __fmul_rn((float)(L + H), 0.5f);
+    uint32_t klo = smin, clo = P2_S, chi = 0;
+    uint64_t khi = (uint64_t)smax + 1ull;
+    int it = 0;
+    uint32_t hits = 0;
+    auto probe = [&](uint32_t T) -> bool {  // group-uniform
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < P2_CHUNK; ++q) m += sk[q] >= T ? 1u : 0u;
+        hits = group_red1<R_ADD>(c, m);
+        ++it;
+        if (hits >= (uint32_t)L && hits <= (uint32_t)H) return true;
+        if (hits > (uint32_t)H) {
+            klo = T;
+            clo = hits;
+        } else {
+            khi = T;
+            chi = hits;
+        }
+        return false;
+    };
+    int exitk = GVR_P2_WINDOW;
+    uint32_t T = 0;
+    bool found = false;
+    if (isfinite(pmean)) {
+        const uint32_t t0 = f2key(pmean);
+        if (t0 > klo && (uint64_t)t0 < khi) {
+            T = t0;
+            found = probe(t0);
+            if (!found) {
+                const uint32_t t1 = hits < (uint32_t)L ? kmn : kmx;
+                if (t1 > klo && (uint64_t)t1 < khi) {
+                    T = t1;
+                    found = probe(t1);
+                }
+            }
         }
     }
-    group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
-    if (cnt == 0) {
-        // no valid guess: deterministic stride sample of M values
-        kmn = 0xffffffffu;
-        kmx = 0u;
-        sum = sq = 0.f;
-        const int M = min(KMAX, p.n);
-        for (int j = c.tid; j < M; j += G::N) {
-            const int q = (int)(((int64_t)j * p.n) / M);
-            const float v = ld_gather(p.x + q);
-            const uint32_t kv = f2key(v);
-            kmn = min(kmn, kv);
-            kmx = max(kmx, kv);
-            ++cnt;
-            sum += v;
-            sq += v * v;
+    for (int secants = 0; !found; ++secants) {
+        if (khi - klo < 2) {
+            exitk = GVR_P2_TIES;
+            break;
         }
-        group_red4<R_MIN, R_MAX, R_ADD, R_ADD>(c, kmn, kmx, cnt, unused);
+        if (it >= P2_MAX_ITERS) {
+            exitk = GVR_P2_EXHAUSTED;
+            break;
+        }
+        T = secant_step(klo, clo, khi, chi, ft, secants == 0, secants >= prm.max_secant);
+        found = probe(T);
     }
-    group_fsum2(c, sum, sq);
-    const float pmean = sum / (float)cnt;
-    const float var = fmaxf(sq / (float)cnt - pmean * pmean, 0.f);
-    // width of the collect threshold (R22): rows with K/N > 1/8 need a wider margin
-    // (scripts/sigma_by_n.py: at N = 8192 sigma 0.3 undershoots on 88% of rows, 0.7 on none)
-    float sg = prm.collect_sigma;
-    if (sg >= 0.f && p.n < 8 * k) sg = fmaxf(sg, 0.7f);
-    const float tcf = pmean - sg * sqrtf(var);
-    GuessOut g;
-    g.Tc = isfinite(tcf) ? f2key(tcf) : kmn;
-    if (p.n <= GVR_CAP) g.Tc = 0u;  // the whole row fits in B
+    if (!found) {
+        T = klo;
+        hits = clo;
+    }
+    g.Tc = T;
     g.T0 = f2key(pmean);
     g.t0_ok = isfinite(pmean) ? 1 : 0;
-    g.tmin = (stride == 1 && cnt == (uint32_t)k && kmn < g.Tc) ? kmn : 0u;
+    g.tmin = (complete && kmn < T) ? kmn : 0u;
+    g.top = max(kmx, smax);
+    g.iters = (int16_t)it;
+    g.exit = (int16_t)exitk;
+    g.scount = (int32_t)hits;
     return g;
 }
 
-// ---------------- Phase 1: guess statistics (Eq. 4)
-// x at the previous step's Top-K positions -> pmin / pmax / pmean plus the second
-// moment; T_c = pmean - sigma * sd (R5), T0 = pmean for Phase 2.  Runs as its
-// own kernel ahead of the streaming kernel: with every row's gathers in flight at once
-// and no streaming traffic in the memory queues, the two dependent round trips (guess
-// indices, then the values) cost one short kernel instead of stalling each row's CTA.
+// ---------------- Phases 1-2 for the batch paths
+// One 256-thread CTA per row, all rows resident at once: with every row's gathers in
+// flight together and no streaming traffic in the memory queues, the dependent round
+// trips (guess indices, then the values and the sample) cost one short kernel instead of
+// stalling each row's streaming CTA.
 constexpr int GUESS_NT = 256;
 using GuessGroup = Group<GUESS_NT, 1>;
 
-//
-// It also schedules the streaming kernel: a strided sample of GUESS_NT row values
-// estimates f(T_c); rows whose estimate exceeds the buffer (poor guesses, which need
-// threshold raises) are put at the front of the row order, the others at the back, so
-// the expensive rows start in the first wave instead of setting the makespan.
+// Row order of the row path (batch_path = 1): rows whose Phase 2 did not end in its
+// window (ties, exhausted) first, so the expensive rows start in the first wave.
 struct RowSched {
     int32_t* order;    // [num_rows]: CTA b of the streaming kernel processes row order[b]
     int32_t* cursors;  // [3]: front / back fill counts, finished streaming CTAs (zero at launch)
 };
-
-constexpr int SQ_N = 1024;  // row samples for the threshold of a poor-guess row
-
-// The rank-th largest of the NS keys in sq (1 <= rank <= NS): most-significant-digit
-// radix select, 8 bits per level over a 256-bin histogram (one bin per thread).
-template <int NS>
-__device__ __forceinline__ uint32_t sample_rank_key(GuessGroup& c, const uint32_t* sq, int32_t* sh, int rank)
-{
-    uint32_t prefix = 0u, pmask = 0u, rem = (uint32_t)rank;
-    c.sync();  // sq complete
-    for (int level = 0; level < 4; ++level) {
-        const int shift = 24 - 8 * level;
-        sh[c.tid] = 0;
-        c.sync();
-#pragma unroll
-        for (int j = 0; j < NS / GUESS_NT; ++j) {
-            const uint32_t kk = sq[c.tid + j * GUESS_NT];
-            if ((kk & pmask) == prefix) atomicAdd(&sh[(kk >> shift) & 255u], 1);
-        }
-        c.sync();
-        const int bin = 255 - c.tid;  // thread t owns bin 255 - t: descending digit order
-        const uint32_t h = (uint32_t)sh[bin];
-        uint32_t tot;
-        const uint32_t ex = group_excl_scan(c, h, tot);
-        if (ex < rem && ex + h >= rem) {
-            c.misc[0] = bin;
-            c.misc[1] = (int)ex;
-        }
-        c.sync();
-        prefix |= (uint32_t)c.misc[0] << shift;
-        pmask |= 255u << shift;
-        rem -= (uint32_t)c.misc[1];
-        c.sync();
-    }
-    return prefix;
-}
 
 __global__ void __launch_bounds__(GUESS_NT)
 gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens,
@@ -765,53 +821,17 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
         asm volatile("prefetch.global.L2 [%0];" ::"l"(prev + (int64_t)r * k + 32 * c.tid));
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
     // batch filter path: a row with no tiles never reaches the filter kernel; it goes to
-    // the ready queue now (the refine kernel hands it on to the fixup list)
+    // the ready queue now (the refine kernel emits it from the row itself)
     if (bq.queue && p.ntiles == 0 && c.tid == 0) st_release(bq.queue + atomicAdd(bq.qctl + Q_TAIL, 1), r + 1);
     if (p.n <= k) {  // trivial row: no guess needed (block-uniform); scheduled last
         if (c.tid == 0 && !bq.queue) sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
         return;
     }
-    // one strided row sample per thread, gathered alongside the guess values
-    const float xs = ld_gather(p.x + (int)(((int64_t)c.tid * p.n) / GUESS_NT));
-    const int32_t* pr = prev ? prev + (int64_t)r * k : nullptr;
-    GuessOut g = phase1_guess(c, p, pr, k, prm);
-    const uint32_t hits = group_red1<R_ADD>(c, f2key(xs) >= g.Tc ? 1u : 0u);
-    const bool heavy = (double)hits * p.n > (double)GVR_CAP * GUESS_NT;  // estimated f(T_c) > capacity
-    if (heavy && p.n >= 4 * k) {
-        // poor guess (low Top-K overlap, e.g. layers 0-1, or late MTP
-        // draft tokens): its statistics put T_c below the K-th value by more than the
-        // buffer.  Take the threshold from strided row samples instead: the r-th largest
-        // sample key, r chosen so that about f_s elements are expected at or above it
-        // (sampling error of f(T_s)/f_s ~ 1/sqrt(r); an undershoot only costs the row a
-        // second stream).  Far above the buffer (estimate > 4x): 1024 new samples and
-        // f_s = 2.5 k + 512; otherwise the 256 samples already gathered (no second round
-        // trip) and a safer f_s = 4 k.
-        __shared__ uint32_t sq[SQ_N];
-        __shared__ int32_t sh[GUESS_NT];
-        const bool poor = (double)hits * p.n > 4.0 * GVR_CAP * GUESS_NT;
-        uint32_t Ts;
-        if (poor) {
-#pragma unroll
-            for (int j = 0; j < SQ_N / GUESS_NT; ++j) {
-                const int q = c.tid + j * GUESS_NT;
-                sq[q] = f2key(ld_gather(p.x + (int)(((int64_t)q * p.n) / SQ_N)));
-            }
-            const int rank = (int)ceil((2.5 * k + 512.0) * SQ_N / p.n);
-            Ts = sample_rank_key<SQ_N>(c, sq, sh, rank < SQ_N ? rank : SQ_N);
-        } else {
-            sq[c.tid] = f2key(xs);
-            const int rank = (int)ceil(4.0 * k * GUESS_NT / p.n);
-            Ts = sample_rank_key<GUESS_NT>(c, sq, sh, rank < GUESS_NT ? rank : GUESS_NT);
-        }
-        if (Ts > g.Tc) {
-            g.Tc = Ts;
-            g.tmin = 0u;
-        }
-    }
+    const GuessOut g = phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm);
     if (c.tid == 0) {
         gp[r] = g;
-        if (!bq.queue) {  // the row path's order: heavy rows first (the filter path needs none)
-            if (heavy)
+        if (!bq.queue) {
+            if (g.exit == GVR_P2_TIES || g.exit == GVR_P2_EXHAUSTED)
                 sched.order[atomicAdd(sched.cursors, 1)] = r;
             else
                 sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
@@ -832,13 +852,16 @@ __device__ __forceinline__ void fixup_done(int32_t* ctl, const BatchQueue& bq, i
     }
 }
 
-// One row, the whole path: Phase 1 (or its hand-off), the streaming pass, Phases 2-4 and
-// the ordered output, with every fallback.  A CTA calls it once per row (reinit: the ring
-// barriers were used by a previous row of this CTA).
+// One row, the whole path: Phases 1-2 (or their hand-off), the streaming pass, Phases 3-4
+// and the ordered output, with every fallback.  A CTA calls it once per row (reinit: the
+// ring barriers were used by a previous row of this CTA).  short_known: an earlier pass
+// (the filter kernel) already found f(T_c) < K, so the row is streamed at once at the
+// second-pass threshold (R30).
 __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64_t stride,
                                       const int32_t* __restrict__ row_lens, int k, int32_t* out, float* out_val,
                                       gvr_row_stats* stats, const GvrParams& prm, const GuessOut* __restrict__ gp,
-                                      const int32_t* prev, long long* phase_ts, int r, bool reinit)
+                                      const int32_t* prev, long long* phase_ts, int r, bool reinit,
+                                      bool short_known = false)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
@@ -867,18 +890,18 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
     int st[4] = {0, 0, 0, 0};
     int done_kind = GVR_DONE_CONVERGED, passes = 1, raises = 0, ftc_stat = 0;
     long long tsr[TS_N] = {ts0, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
+    GuessOut gq{};
     if (p.n <= k) {
         c.sync();
         small_row_emit(c, B, Wk, g, k, o, ov);
         done_kind = GVR_DONE_TRIVIAL;
         st[2] = p.n;
     } else {
-        // ---------------- Phase 1: in gvr_guess_kernel (split) or here (fused)
-        const GuessOut gq = gp ? gp[r] : phase1_guess(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm);
+        // ---------------- Phases 1-2: in gvr_guess_kernel (batch paths) or here (fused)
+        gq = gp ? gp[r] : phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm);
         RowMeta m;
-        m.Tc = gq.Tc;
-        m.T0 = gq.T0;
-        m.t0_ok = gq.t0_ok != 0;
+        m.Tc = short_known ? gq.tmin : gq.Tc;
+        if (short_known) passes = 2;
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         // ---------------- streaming pass (HBM read once, TMA ring)
         uint32_t kmax = 0u, extras = 0u, tie_key = 0u;
@@ -895,8 +918,15 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
             done_kind = GVR_DONE_TIEFILL;
             ++passes;
             tiefill_emit(c, B, Wk, g, tie_key, m.ftc, K, k, o, ov);
+        } else if (rc == 0 && m.ftc < (uint32_t)K && short_known) {
+            // the second-pass threshold was short as well (only massive ties can do that):
+            // exact radix select + ordered tie fill
+            const RadixResult rr = radix_select_global(c, Wk, g, (uint32_t)K, false);
+            passes += rr.rounds + 1;
+            done_kind = GVR_DONE_TIEFILL;
+            tiefill_emit(c, B, Wk, g, rr.prefix, rr.above, K, k, o, ov);
         } else if (rc == 0 && m.ftc < (uint32_t)K) {
-            // f(T_c) < K (the guess overshot the K-th value): stream the row once more at
+            // f(T_c) < K (the threshold overshot the K-th value): stream the row once more at
             // a threshold that cannot undershoot — pmin of a complete guess, else -inf —
             // with the usual raises keeping >= K (R30); bounded at two HBM passes
             c.sync();
@@ -925,7 +955,7 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
                 tiefill_emit(c, B, Wk, g, tie2, m.ftc, K, k, o, ov);
             } else if (rc2 == 0 && m.ftc >= (uint32_t)K) {
                 ftc_stat = (int)m.ftc;
-                refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
+                refine_row(c, B, Wk, m, k, o, ov, st, phase_ts ? tsr : nullptr);
                 if (st[3]) {
                     done_kind = GVR_DONE_TIEFILL;
                     ++passes;
@@ -946,7 +976,7 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
             tiefill_emit(c, B, Wk, g, rr.prefix, rr.above, K, k, o, ov);
         } else {
             ftc_stat = (int)m.ftc;
-            refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
+            refine_row(c, B, Wk, m, k, o, ov, st, phase_ts ? tsr : nullptr);
             if (st[3]) {
                 // huge tie group at T*: ordered tie fill from global memory (R13)
                 done_kind = GVR_DONE_TIEFILL;
@@ -958,7 +988,7 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
     if (c.tid == 0) {
         if (stats) {
             gvr_row_stats s;
-            s.secant_iters = st[0];
+            s.secant_iters = gq.iters;
             s.snap_iters = st[1];
             s.cand_count = st[2];
             s.done_kind = done_kind;
@@ -966,6 +996,10 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
             s.raises = raises;
             s.buffer_count = ftc_stat;
             s.cluster = 1;
+            s.phase2_exit = gq.exit;
+            s.sample_count = gq.scount;
+            s.tc_key = gq.Tc;
+            s.reserved = 0;
             stats[r] = s;
         }
         if (phase_ts) {
@@ -1006,8 +1040,11 @@ gvr_fixup_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the refine grid's fixup list is complete
     const int nfix = ld_relaxed(bq.qctl + Q_NFIX);
     for (int li = (int)blockIdx.x; li < nfix; li += (int)gridDim.x)
-        topk_row(scores, stride, row_lens, k, out, out_val, stats, prm, gp, prev, phase_ts, __ldcg(bq.fixlist + li),
-                 li != (int)blockIdx.x);
+    {
+        const uint32_t e = (uint32_t)__ldcg(bq.fixlist + li);  // row | (f(T_c) < K known) << 31
+        topk_row(scores, stride, row_lens, k, out, out_val, stats, prm, gp, prev, phase_ts, (int)(e & 0x7fffffffu),
+                 li != (int)blockIdx.x, (e >> 31) != 0u);
+    }
     fixup_done(ctl, bq, threadIdx.x);
 }
 
@@ -1146,6 +1183,7 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
     int st[4] = {0, 0, 0, 0};
     int done_kind = GVR_DONE_CONVERGED, passes = 1, raises = 0, ftc_stat = 0;
     long long tsr[TS_N] = {ts0, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
+    GuessOut gq{};
     if (pw.n <= k) {  // cluster-uniform: the leader emits the whole row
         if (g != 0) return;
         c.sync();
@@ -1154,7 +1192,7 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
         st[2] = pw.n;
     } else {
         // ---------------- Phase 1 (every CTA, identical result) and the slice stream
-        const GuessOut gq = phase1_guess(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm);
+        gq = phase12(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm);
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         uint32_t Tc = gq.Tc, kmax = 0u, extras = 0u, Tm = 0u, kmx = 0u, T = 0u, tot = 0, pre = 0;
         int fill = 0, raises_all = 0;
@@ -1256,10 +1294,8 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
             m.ftc = tot;
             m.kmax = kmx;
             m.extras = 0u;  // the merge compared exact keys
-            m.T0 = gq.T0;
-            m.t0_ok = gq.t0_ok != 0;
             ftc_stat = (int)tot;
-            refine_row(c, B, Wk, m, prm, k, o, ov, st, phase_ts ? tsr : nullptr);
+            refine_row(c, B, Wk, m, k, o, ov, st, phase_ts ? tsr : nullptr);
             if (st[3]) {
                 done_kind = GVR_DONE_TIEFILL;
                 ++passes;
@@ -1279,7 +1315,7 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
     if (c.tid == 0) {
         if (stats) {
             gvr_row_stats sr;
-            sr.secant_iters = st[0];
+            sr.secant_iters = gq.iters;
             sr.snap_iters = st[1];
             sr.cand_count = st[2];
             sr.done_kind = done_kind;
@@ -1287,6 +1323,10 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
             sr.raises = raises;
             sr.buffer_count = ftc_stat;
             sr.cluster = G;
+            sr.phase2_exit = gq.exit;
+            sr.sample_count = gq.scount;
+            sr.tc_key = gq.Tc;
+            sr.reserved = 0;
             stats[r] = sr;
         }
         if (phase_ts) {

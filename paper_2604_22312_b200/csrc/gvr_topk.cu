@@ -229,7 +229,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     if (prev_topk && prev_topk != out_idx && ranges_overlap(prev_topk, bytes, out_idx, bytes))
         return GVR_ERR_INVALID_ARGUMENT;
     GvrParams prm;
-    prm.collect_sigma = 0.3f;  // DESIGN.md R22: measured sweep (cfg2, cfg4)
+    prm.window_z = P2_Z_DEFAULT;  // DESIGN.md R35
     prm.max_secant = 8;
 #ifndef GVR_DEFAULT_GUESS_STRIDE
 #define GVR_DEFAULT_GUESS_STRIDE 4  // DESIGN.md R29
@@ -237,7 +237,8 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     prm.guess_stride = GVR_DEFAULT_GUESS_STRIDE;
     if (opt) {
         if (opt->guess_stride > 0) prm.guess_stride = opt->guess_stride;
-        if (opt->collect_sigma == opt->collect_sigma) prm.collect_sigma = opt->collect_sigma;
+        // 0 / NaN = default; a negative z aims below the K-th value (tests of R30)
+        if (opt->window_z == opt->window_z && opt->window_z != 0.f) prm.window_z = opt->window_z;
         if (opt->max_secant_iters > 0) prm.max_secant = opt->max_secant_iters;
     }
     if ((st = set_smem(gvr_topk_kernel, GVR_SMEM_BYTES)) != GVR_OK) return st;

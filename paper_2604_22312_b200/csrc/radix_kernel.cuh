@@ -93,6 +93,10 @@ radix_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         s.raises = 0;
         s.buffer_count = 0;
         s.cluster = 1;
+        s.phase2_exit = GVR_P2_ALL;
+        s.sample_count = 0;
+        s.tc_key = 0u;
+        s.reserved = 0;
         stats[r] = s;
     }
 }

@@ -15,9 +15,8 @@
 //   * rows this cannot finish — no tiles (len <= k or tiny rows), a list that overflowed its
 //     region or holds fewer than K keys >= T_c (the guess overshot), a K-th bin crowded by
 //     ties — go to the fixup list, worked off by gvr_topk_kernel in fixup mode.
-// The paper's Phase 2 (secant narrowing to C candidates) exists to fit
-// the candidates in shared memory; here the list stays in L2 and the histogram covers it
-// directly, so f(T_c) is the only count (secant_iters = 1).
+// Phase 2 (the secant search) ran in gvr_guess_kernel over the row
+// sample, so the list is {key >= T_c} with K <= f(T_c) ~ 1.3-2 K (R34-R36).
 #pragma once
 #include "filter_kernel.cuh"
 
@@ -326,10 +325,14 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         }
         if (c.tid == 0) {
             if (!ok) {
-                bq.fixlist[atomicAdd(bq.qctl + Q_NFIX, 1)] = r;
+                // a complete list with fewer than K keys >= T_c: the fixup streams the row at
+                // the second-pass threshold directly (flag bit 31)
+                const bool short_list = p.ntiles > 0 && p.n > k && total >= 0 && total < K;
+                bq.fixlist[atomicAdd(bq.qctl + Q_NFIX, 1)] = (int32_t)((uint32_t)r | (short_list ? 0x80000000u : 0u));
             } else if (stats) {
+                const GuessOut g = trivial ? GuessOut{} : gp[r];
                 gvr_row_stats s;
-                s.secant_iters = trivial ? 0 : 1;  // f(T_c), counted from the list
+                s.secant_iters = g.iters;  // Phase-2 probes (gvr_guess_kernel)
                 s.snap_iters = 0;
                 s.cand_count = trivial ? p.n : ftc;
                 s.done_kind = trivial ? GVR_DONE_TRIVIAL : GVR_DONE_CONVERGED;
@@ -337,6 +340,10 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 s.raises = levels > 1 ? levels - 1 : 0;  // Phase-4 histogram narrowings (R32)
                 s.buffer_count = trivial ? 0 : ftc;
                 s.cluster = 1;
+                s.phase2_exit = g.exit;
+                s.sample_count = g.scount;
+                s.tc_key = g.Tc;
+                s.reserved = 0;
                 stats[r] = s;
             }
             if (phase_ts && ok) {

@@ -86,13 +86,17 @@ def g_delta(n: int, inv_freq: torch.Tensor | None = None) -> np.ndarray:
     return 2.0 * np.cos(np.outer(d, th)).sum(axis=1)
 
 
-def static_prior(n: int, k: int = 2048) -> np.ndarray:
-    """Eq. 3 static prior: positions m whose relative distance
-    Delta = n-1-m is among the k largest g(Delta).  Input generation only."""
-    g = g_delta(n)
+def static_prior(n: int, k: int = 2048, query_pos: int | None = None) -> np.ndarray:
+    """Eq. 3 static prior: the k positions m whose relative distance
+    Delta = |query_pos - m| to the query has the largest g(Delta).  The query sits at the
+    newest position n - 1 by default (the Eq.-1 decode rows, IndexerLayer); the App.-E
+    listing rotates it at position 0 (appendix_e_row: query_pos=0).  Input generation
+    only."""
+    qp = n - 1 if query_pos is None else int(query_pos)
+    m = np.arange(n, dtype=np.int64)
+    g = g_delta(n)[np.abs(qp - m)]
     kk = min(k, n)
-    order = np.argsort(-g, kind="stable")[:kk]  # Delta values
-    pos = (n - 1 - order).astype(np.int32)
+    pos = np.argsort(-g, kind="stable")[:kk].astype(np.int32)
     out = np.full(k, -1, dtype=np.int32)
     out[:kk] = pos
     return out

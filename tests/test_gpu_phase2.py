@@ -1,0 +1,214 @@
+"""GPU: Phase 2 (the secant search of Eq. 6 over the row sample, R34-R36) and
+the batch paths at the sizes and guess qualities the round-1 tests did not reach.
+
+* The kernel's per-row Phase-2 statistics — T_c (as a key), I (probes), the exit kind
+  and the sample hits at T_c — equal the CPU replay (oracle/phase2_replay.py) bit for bit,
+  on every launch path (fused, cluster, batch filter, batch row).
+* High-correlation decode rows (rho = 0.95 / 0.98 / 0.995, alpha up to ~0.8) on the
+  filter path: exact, one HBM pass, no fixup rows.
+* Filter-path batches at N = 131,072 (cfg5-shaped) and 262,144, a batch of massive ties
+  that runs through the fixup kernel, the snap branch of Phase 4, MTP draft rows.
+Every output is compared with the oracle element by element."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import phase2_replay as P2
+import synth
+
+pytestmark = pytest.mark.gpu
+K = 2048
+F = None  # STATS_FIELDS, set by the fixture
+
+
+@pytest.fixture(scope="module")
+def gvr(cuda_device):
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2604_22312_b200 as m
+    global F
+    F = m.STATS_FIELDS
+    return m
+
+
+def _col(st, name):
+    return st[:, F.index(name)]
+
+
+def _run(gvr, scores, lens, prev, k=K, opts=None):
+    import torch
+    idx, _, st = gvr.topk_ex(scores, k, row_lens=lens, prev=prev, values=False, options=opts)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), st.cpu().numpy()
+
+
+def _assert_exact(got, ref, st=None):
+    bad = np.argwhere((got != ref).any(axis=1))[:, 0]
+    assert bad.size == 0, f"{bad.size} rows differ, first {bad[:5].tolist()}" + (
+        "" if st is None else f" stats {st[bad[:3]].tolist()}")
+
+
+def _heads(R, stride):
+    """Scalars before each row's first 16-byte boundary (torch bases are 16-B aligned)."""
+    return [((16 - ((r * stride * 4) & 15)) & 15) >> 2 for r in range(R)]
+
+
+def _assert_replay(host, lens, prev, st, k=K, stride_guess=4, rows=None):
+    """Kernel Phase-2 statistics == the CPU replay, row by row."""
+    R, S = host.shape
+    heads = _heads(R, S)
+    rows = range(R) if rows is None else rows
+    for r in rows:
+        n = int(lens[r])
+        if n <= k:
+            continue
+        rep = P2.replay_row(host[r, :n], None if prev is None else prev[r], k, head=heads[r], stride=stride_guess)
+        got = (int(_col(st, "tc_key")[r]) & 0xFFFFFFFF, int(_col(st, "secant_iters")[r]),
+               int(_col(st, "phase2_exit")[r]), int(_col(st, "sample_count")[r]))
+        exp = (rep["Tc"], rep["I"], rep["done"], rep["count"] if rep["done"] else 0)
+        if rep["done"] == P2.DONE_ALL:
+            exp = (0, 0, 0, 0)
+        assert got == exp, f"row {r} n {n}: kernel {got} replay {exp}"
+
+
+def _decode_batch(requests, layers, n, seed, rho=None, draft=1):
+    import torch
+    from bench import make_decode_batch
+    b = make_decode_batch(requests, layers, n, torch.device("cuda:0"), seed=seed, draft=draft, rho=rho)
+    torch.cuda.synchronize()
+    return b
+
+
+# ------------------------------------------------------------------ replay parity
+@pytest.mark.parametrize("n", [8192, 40_000, 100_000, 262_144])
+def test_phase2_stats_match_replay_fused_and_cluster(gvr, n):
+    """Few rows (fused kernel, or a cluster per row when long): Phases 1-2 run inside the
+    row's CTA; every CTA of a cluster computes the same T_c."""
+    import torch
+    rows, prevs = [], []
+    for i, rho in enumerate((0.9, 0.0, 0.97)):
+        p, c = synth.decode_pair(n, rho, seed=synth.splitmix64(2100, n, i))
+        rows.append(c.numpy())
+        prevs.append(oracle.topk(p.numpy(), K))
+    rows.append(synth.dist_row("lognormal", n, seed=2101))
+    prevs.append(np.full(K, -1, np.int32))  # no valid guess: sample statistics
+    host = np.stack(rows)
+    lens = np.full(len(rows), n, np.int32)
+    prev = np.stack(prevs).astype(np.int32)
+    dev = torch.device("cuda:0")
+    got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev))
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    _assert_replay(host, lens, prev, st)
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_phase2_stats_match_replay_batch_paths(gvr, path):
+    """More than one wave (guess kernel + filter / row path), ragged lengths and strides
+    that misalign rows, mixed guess kinds (prev step, random, adversarial, none)."""
+    import torch
+    rng = np.random.default_rng(2200 + path)
+    R, S = 320, 70_001
+    lens = rng.integers(3_000, S + 1, size=R).astype(np.int32)
+    host = np.zeros((R, S), np.float32)
+    prev = np.full((R, K), -1, np.int32)
+    for r in range(R):
+        n = int(lens[r])
+        row = synth.dist_row(("normal", "lognormal", "uniform", "heavy_tail")[r % 4], n, seed=2201 + r)
+        host[r, :n] = row
+        kind = ("prev", "random", "adversarial", "none")[r % 4]
+        noisy = row + 0.3 * rng.standard_normal(n).astype(np.float32) * np.float32(np.std(row) + 1e-6)
+        g = synth.guess(kind, row, K, 2202 + r, prev_topk=oracle.topk(noisy, K))
+        if g is not None:
+            prev[r] = g
+    dev = torch.device("cuda:0")
+    got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev),
+                   opts=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    _assert_replay(host, lens, prev, st)
+
+
+# ------------------------------------------------------------------ high alpha
+@pytest.mark.parametrize("rho", [0.95, 0.98, 0.995])
+def test_high_alpha_filter_path_one_pass_no_fixup(gvr, rho):
+    """Strongly correlated decode steps (alpha ~0.55-0.8, above the paper's 0.35-0.50 band,
+    PAPER.md:275-277): Phase 2 keeps K <= f(T_c) on both sides of pmean, so every row of
+    a 300-row N=100K filter-path batch is exact in one HBM pass with no fixup."""
+    b = _decode_batch(5, 60, 100_000, seed=synth.splitmix64(2300, int(rho * 1000)), rho=rho)
+    got, st = _run(gvr, b["scores"], b["row_lens"], b["prev"])
+    host = b["scores"].cpu().numpy()
+    lens = b["row_lens"].cpu().numpy()
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    assert (_col(st, "global_passes") == 1).all() and (_col(st, "done_kind") == 1).all(), st[:3].tolist()
+    assert (_col(st, "phase2_exit") == 1).all()
+    assert (_col(st, "buffer_count") >= K).all()
+    # alpha really is high: the guess overlaps the exact Top-K
+    prev = b["prev"].cpu().numpy()
+    ref = oracle.topk_batched(host[:20], K, row_lens=lens[:20])
+    alpha = np.mean([len(np.intersect1d(prev[r], ref[r])) / K for r in range(20)])
+    assert alpha > 0.5
+    _assert_replay(host, lens, prev, st, rows=range(0, 300, 37))
+
+
+# ------------------------------------------------------------------ sizes on the filter path
+@pytest.mark.parametrize("n", [131_072, 262_144])
+def test_filter_path_long_rows(gvr, n):
+    """cfg5-shaped rows (N = 131,072) and N = 262,144 in 300-row batches: more than one
+    wave, so the filter path (guess, filter, refine, fixup kernels) runs them."""
+    b = _decode_batch(5, 60, n, seed=synth.splitmix64(2400, n))
+    got, st = _run(gvr, b["scores"], b["row_lens"], b["prev"])
+    host = b["scores"].cpu().numpy()
+    lens = b["row_lens"].cpu().numpy()
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    assert (_col(st, "global_passes") == 1).all()
+    assert (_col(st, "cluster") == 1).all()
+
+
+def test_filter_path_mtp_draft_rows(gvr):
+    """cfg4-shaped rows: 4 draft tokens per request, each one more decode step past the
+    shared guess (alpha decays along the draft), N + j keys."""
+    b = _decode_batch(16, 5, 100_000, seed=2450, draft=4)
+    got, st = _run(gvr, b["scores"], b["row_lens"], b["prev"])
+    host = b["scores"].cpu().numpy()
+    lens = b["row_lens"].cpu().numpy()
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    assert (_col(st, "global_passes") == 1).all()
+
+
+def test_massive_ties_batch_through_fixup(gvr):
+    """300 rows of all-equal / few-distinct / 90%-tied values: the refine kernel cannot
+    finish them from their lists (crowded K-th bin), the fixup kernel streams them again
+    and fills the ties in index order; exact."""
+    import torch
+    R, n = 300, 50_000
+    kinds = ("all_equal", "few_distinct", "ties90")
+    rows = [synth.dist_row(kinds[r % 3], n - (r % 7), seed=2500 + r) for r in range(R)]
+    S = n
+    host = np.zeros((R, S), np.float32)
+    lens = np.array([r.size for r in rows], np.int32)
+    for r, row in enumerate(rows):
+        host[r, :row.size] = row
+    prev = np.stack([synth.guess("random", rows[r], K, 2501 + r) for r in range(R)]).astype(np.int32)
+    dev = torch.device("cuda:0")
+    got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev))
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    assert (_col(st, "done_kind") == 2).sum() > 0  # tie fill ran
+
+
+def test_snap_branch_runs(gvr):
+    """A tie group of 300 at the row maximum crowds one bin above the K-th one, so the
+    sorted-bin shortcut (R28) is refused and Phase 4's snap iterations
+    find T*: snap_iters > 0, exact."""
+    import torch
+    rows = []
+    for i in range(3):
+        row = synth.dist_row("normal", 60_000, seed=2600 + i)
+        row[np.random.default_rng(i).choice(60_000, 300, replace=False)] = np.float32(50.0)
+        rows.append(row)
+    host = np.stack(rows)
+    lens = np.full(3, 60_000, np.int32)
+    prev = np.stack([synth.guess("random", r, K, 2601) for r in rows]).astype(np.int32)
+    dev = torch.device("cuda:0")
+    got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev),
+                   opts=gvr.GvrOptions(float("nan"), 0, 1, 0))  # one CTA per row (the row kernel)
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    assert (_col(st, "snap_iters") > 0).all(), st.tolist()

@@ -36,6 +36,22 @@ def test_static_prior_valid_positions():
     assert p.min() >= 0 and p.max() == n - 1  # Delta = 0 is the global maximum of g
     short = synth.static_prior(100, 2048)
     assert (short[:100] >= 0).all() and (short[100:] == -1).all()
+    p0 = synth.static_prior(n, 2048, query_pos=0)
+    assert 0 in set(p0.tolist())  # Delta = 0 is position 0 when the query sits there
+    assert sorted(p0.tolist()) == sorted((n - 1 - p).tolist())  # mirror image
+
+
+def test_static_prior_matches_appendix_e_rows():
+    """App.-E rows (query at position 0) are dominated by g(Delta):
+    the prior built for query_pos=0 overlaps the exact Top-K far above chance (K/N),
+    the mirrored one (query at the end) does not."""
+    import oracle
+    n, k = 16384, 2048
+    row = synth.appendix_e_row(n, seed=5).numpy()
+    top = set(oracle.topk(row, k).tolist())
+    a0 = len(top & set(synth.static_prior(n, k, query_pos=0).tolist())) / k
+    a_end = len(top & set(synth.static_prior(n, k).tolist())) / k
+    assert a0 > 0.5 > a_end
 
 
 def test_rope_is_a_rotation_and_relative():
