@@ -98,26 +98,33 @@ def tree_sum(vals: np.ndarray) -> np.float32:
     return butterfly(lanes)
 
 
+def guessed_ranks(k: int, stride: int) -> np.ndarray:
+    """Ranks of the guess list used by Phase 1 (R29), slot i = 0..2047 (thread i % 256,
+    register i // 256): m_i = 8 stride floor(i / 8) + i % 8, used while m_i < k —
+    blocks of 8 consecutive ranks every 8 stride ranks; stride 1 = every rank."""
+    i = np.arange(GUESS_THREADS * GUESS_SLOTS, dtype=np.int64)
+    return 8 * stride * (i >> 3) + (i & 7)
+
+
 def phase1(x: np.ndarray, guess, k: int, stride: int):
     """pmin, pmax (keys) and pmean (Eq. 4) over the valid guessed
-    positions q = guess[m * stride], m < ceil(k / stride) (R29); positions outside
-    [0, n) are ignored (R7).  Values in thread order: thread t holds m = t + 256 j.
-    Returns (pmin_key, pmax_key, pmean, count); count 0 means no valid guess."""
+    positions q = guess[m_i] (guessed_ranks); positions outside [0, n) are ignored (R7).
+    Returns (pmin_key, pmax_key, pmean, count), or None when no position is valid."""
     n = x.size
     if guess is None:
         return None
     g = np.asarray(guess, dtype=np.int64)
-    M = (k + stride - 1) // stride
-    slots = GUESS_THREADS * GUESS_SLOTS  # thread t holds slots t + 256 j, j < 8
-    pos = np.full(slots, -1, dtype=np.int64)
-    pos[:M] = g[np.arange(M) * stride]
+    m = guessed_ranks(k, stride)
+    pos = np.full(m.size, -1, dtype=np.int64)
+    use = m < k
+    pos[use] = g[m[use]]
     ok = (pos >= 0) & (pos < n)
     vals = np.where(ok, x[np.clip(pos, 0, n - 1)], np.float32(0)).astype(np.float32)
     if not ok.any():
         return None
     kk = keys(vals[ok])
-    # slot m = t + 256 j belongs to thread t; invalid slots add +0.0
-    s = tree_sum(vals.reshape(-1, GUESS_THREADS).T)
+    # slot i = t + 256 j belongs to thread t; invalid slots add +0
+    s = tree_sum(vals.reshape(GUESS_SLOTS, GUESS_THREADS).T)
     cnt = int(ok.sum())
     pmean = f32(s / f32(cnt))
     return int(kk.min()), int(kk.max()), pmean, cnt
@@ -204,7 +211,7 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
             return T, it, DONE_WINDOW, r
 
 
-def replay_row(x: np.ndarray, guess, k: int, head: int = 0, stride: int = 4, z=Z, max_secant: int = MAX_SECANT):
+def replay_row(x: np.ndarray, guess, k: int, head: int = 0, stride: int = 8, z=Z, max_secant: int = MAX_SECANT):
     """Phases 1-2 of one row as the guess kernel runs them (head: the row's scalars before
     its first 16-byte boundary; stride: the guess stride, used for n >= 32 k).  Returns a
     dict with the collect threshold key Tc, I, done (Phase-2 exit), window (L, H), the

@@ -88,15 +88,15 @@ __device__ __forceinline__ long long sm_id()
 // What Phases 1-2 (phase12) hand to the streaming step, per row (32 bytes).
 struct GuessOut {
     uint32_t Tc;     // collect threshold key (Phase 2 result)
-    uint32_t T0;     // f2key(pmean), the Phase-2 start
+    uint32_t pad;
     uint32_t tmin;   // second-pass threshold: pmin when all k guesses were gathered and
                      // valid (then f(pmin) >= k for distinct guesses), else 0 (everything)
     uint32_t top;    // max(pmax, sample max) key
-    int32_t t0_ok;   // pmean finite
+    uint32_t T0;     // f2key(pmean), the Phase-2 start
     int16_t iters;   // Phase-2 probes I
     int16_t exit;    // gvr_phase2_exit
     int32_t scount;  // sample hits at T_c
-    int32_t pad;
+    int32_t t0_ok;   // pmean finite
 };
 static_assert(sizeof(GuessOut) == 32, "GuessOut layout");
 
@@ -620,8 +620,9 @@ constexpr float P2_Z_DEFAULT = 4.5f;
 // Phases 1-2 for one row by a 256-thread group (R7, R8-R12,
 // R19, R29, R34-R36).  Every fp32 operation is explicit round-to-nearest in a fixed
 // order, so the CPU replay reproduces T_c, I and the exit kind bit for bit.
-//   Phase 1: the guessed values x[q], q = prev[m * stride] for m < ceil(k / stride)
-//     (thread t holds m = t + 256 j) -> pmin / pmax (keys), pmean = sum / count (Eq. 4).
+//   Phase 1: the guessed values x[q], q = prev[m] for the guessed ranks m of slots
+//     i = t + 256 j (thread t): m_i = 8 gs floor(i / 8) + i % 8 < k (R29) -> pmin / pmax
+//     (keys), pmean = sum / count (Eq. 4).
 //     No valid guess -> the statistics of the row sample.
 //   Sample: chunk t (16 contiguous floats of the 16-byte aligned body, chunk start
 //     16 * floor(t * nch / 256) of nch = body / 16 chunks) in registers, as keys.
@@ -638,7 +639,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     static_assert(G::N == 256, "one sample chunk per thread");
     constexpr int GPT = KMAX / G::N;  // 8 guessed positions per thread
     GuessOut g;
-    g.pad = 0;
+    g.pad = 0u;
     if (p.n <= GVR_CAP) {  // the whole row fits in B: collect everything, no search
         g.Tc = 0u;
         g.T0 = 0u;
@@ -650,17 +651,32 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
         g.scount = 0;
         return g;
     }
-    // ---- loads: the guessed values (two dependent round trips) and the sample chunk
-    const int stride = p.n >= 32 * k ? prm.guess_stride : 1;  // R29
+    // ---- loads: the sample chunk, the guess indices, then the guessed values
+    const int nch = p.nfl / P2_CHUNK;  // >= 376 for n > GVR_CAP
+    const float4* sp4 =
+        reinterpret_cast<const float4*>(p.x + p.head + P2_CHUNK * (int)(((int64_t)c.tid * nch) >> 8));
+    float sv[P2_CHUNK];
+#pragma unroll
+    for (int q = 0; q < P2_CHUNK / 4; ++q) {
+        const float4 v = ldg_sample(sp4 + q);
+        sv[4 * q] = v.x;
+        sv[4 * q + 1] = v.y;
+        sv[4 * q + 2] = v.z;
+        sv[4 * q + 3] = v.w;
+    }
+    // slot i = tid + 256 j holds guessed rank m_i = 8 gs (i / 8) + i % 8 when m_i < k:
+    // blocks of 8 consecutive ranks every 8 gs ranks (one 32-byte sector of indices per
+    // block), gs = guess_stride for rows with n >= 32 k, else 1 (every rank; R29)
+    const int gs = p.n >= 32 * k ? prm.guess_stride : 1;
     float gv[GPT];
     uint32_t valid = 0;
     if (pr) {
-        const int M = (k + stride - 1) / stride;
         int32_t gi[GPT];
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
-            const int m = c.tid + j * G::N;
-            gi[j] = m < M ? __ldg(pr + m * stride) : -1;
+            const int i = c.tid + j * G::N;
+            const int m = 8 * gs * (i >> 3) + (i & 7);
+            gi[j] = m < k ? __ldg(pr + m) : -1;
         }
 #pragma unroll
         for (int j = 0; j < GPT; ++j) {
@@ -673,18 +689,6 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     } else {
 #pragma unroll
         for (int j = 0; j < GPT; ++j) gv[j] = 0.f;
-    }
-    const int nch = p.nfl / P2_CHUNK;  // >= 376 for n > GVR_CAP
-    const float4* sp4 =
-        reinterpret_cast<const float4*>(p.x + p.head + P2_CHUNK * (int)(((int64_t)c.tid * nch) >> 8));
-    float sv[P2_CHUNK];
-#pragma unroll
-    for (int q = 0; q < P2_CHUNK / 4; ++q) {
-        const float4 v = ldg_sample(sp4 + q);
-        sv[4 * q] = v.x;
-        sv[4 * q + 1] = v.y;
-        sv[4 * q + 2] = v.z;
-        sv[4 * q + 3] = v.w;
     }
     uint32_t sk[P2_CHUNK];
     uint32_t smin = 0xffffffffu, smax = 0u;
@@ -709,7 +713,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     }
     group_red4<R_MIN, R_MAX, R_ADD, R_MAX>(c, kmn, kmx, cnt, smax);
     smin = group_red1<R_MIN>(c, smin);
-    bool complete = cnt == (uint32_t)k && stride == 1;
+    bool complete = cnt == (uint32_t)k && gs == 1;
     if (cnt == 0) {  // no valid guess: statistics of the row sample (R7)
         sum = 0.f;
 #pragma unroll
@@ -784,6 +788,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     g.t0_ok = isfinite(pmean) ? 1 : 0;
     g.tmin = (complete && kmn < T) ? kmn : 0u;
     g.top = max(kmx, smax);
+    g.pad = 0u;
     g.iters = (int16_t)it;
     g.exit = (int16_t)exitk;
     g.scount = (int32_t)hits;
@@ -816,9 +821,6 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     GuessGroup c;
     c.init(threadIdx.x, scratch);
     const int r = blockIdx.x;
-    // the guess indices do not depend on the row length: start fetching them into L2 now
-    if (prev && c.tid < (k + 31) / 32)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(prev + (int64_t)r * k + 32 * c.tid));
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
     // batch filter path: a row with no tiles never reaches the filter kernel; it goes to
     // the ready queue now (the refine kernel emits it from the row itself)

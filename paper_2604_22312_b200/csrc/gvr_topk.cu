@@ -1,5 +1,6 @@
 // gvr_topk.cu — C ABI of libgvrtopk.so (declared in include/gvr_topk.h): argument
 // validation, launch configuration and the host-buffer workspace entry point.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -232,7 +233,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     prm.window_z = P2_Z_DEFAULT;  // DESIGN.md R35
     prm.max_secant = 8;
 #ifndef GVR_DEFAULT_GUESS_STRIDE
-#define GVR_DEFAULT_GUESS_STRIDE 4  // DESIGN.md R29
+#define GVR_DEFAULT_GUESS_STRIDE 8  // DESIGN.md R29
 #endif
     prm.guess_stride = GVR_DEFAULT_GUESS_STRIDE;
     if (opt) {
@@ -381,7 +382,8 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     // Serialised when per-kernel events are recorded between them.
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = ev ? 0 : 1;
+    static const bool no_pdl = getenv("GVR_NO_PDL") != nullptr;  // experiments: serialise the kernels
+    pdl[0].val.programmaticStreamSerializationAllowed = (ev || no_pdl) ? 0 : 1;
     auto launch = [&](auto kern, int grid, int threads, int smem_bytes, auto... args) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)grid);

@@ -1,7 +1,13 @@
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# On the GPU box: the GPU test suite (-x) then bench.py lines for the given configs
+# (default cfg2 cfg4 cfg5), results under gpurun_out/.  Usage: bash scripts/gpu_check.sh [notest] [cfg...]
 mkdir -p gpurun_out
-nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 1800 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-tail -3 gpurun_out/smoke.log; tail -30 gpurun_out/pytest_gpu.log; tail -5 gpurun_out/bench.log
+if [ "$1" != "notest" ]; then
+  python -m pytest tests -m gpu -x -q > gpurun_out/gpu_all.log 2>&1; tail -3 gpurun_out/gpu_all.log
+else
+  shift
+fi
+cfgs="${@:-cfg2 cfg4 cfg5}"
+for c in $cfgs; do
+  python bench.py --config $c --no-e2e --no-cpu > gpurun_out/b_$c.json 2>gpurun_out/b_$c.err || tail -5 gpurun_out/b_$c.err
+done

@@ -53,7 +53,7 @@ def _heads(R, stride):
     return [((16 - ((r * stride * 4) & 15)) & 15) >> 2 for r in range(R)]
 
 
-def _assert_replay(host, lens, prev, st, k=K, stride_guess=4, rows=None):
+def _assert_replay(host, lens, prev, st, k=K, stride_guess=8, rows=None):
     """Kernel Phase-2 statistics == the CPU replay, row by row."""
     R, S = host.shape
     heads = _heads(R, S)

@@ -102,6 +102,15 @@ def test_phase1_spec_example():
     assert (P2.unkey(pmin), P2.unkey(pmax), pmean, cnt) == (1.0, 6.0, 3.0, 4)
 
 
+def test_guessed_ranks_blocks():
+    """R29: blocks of 8 consecutive ranks every 8 * stride ranks; stride 1 = all ranks."""
+    assert list(P2.guessed_ranks(K, 1)) == list(range(2048))
+    m = P2.guessed_ranks(K, 8)
+    used = m[m < K]
+    assert used.size == 256 and list(used[:10]) == [0, 1, 2, 3, 4, 5, 6, 7, 64, 65]
+    assert used[-1] == 64 * 31 + 7
+
+
 def test_phase1_ignores_out_of_range_and_strides():
     x = np.arange(1000, dtype=np.float32)
     g = np.full(K, -1, np.int32)
@@ -109,9 +118,12 @@ def test_phase1_ignores_out_of_range_and_strides():
     p = P2.phase1(x, g, K, 1)
     assert p[3] == 5 and P2.unkey(p[0]) == 5 and P2.unkey(p[1]) == 999
     assert p[2] == np.float32((5 + 9 + 11 + 13 + 999) / 5)
-    # stride 2 keeps positions 0, 2, 4, 6 of the guess list: 5, 2000 (out), 11, 13
+    # stride 2 reads ranks 0-7, 16-23, 32-39, ...: rank 8 is skipped, rank 16 is read
+    g[8] = 500
+    g[16] = 700
+    assert P2.phase1(x, g, K, 1)[3] == 7
     p = P2.phase1(x, g, K, 2)
-    assert p[3] == 3 and p[2] == np.float32((5 + 11 + 13) / 3)
+    assert p[3] == 6 and p[2] == np.float32((5 + 9 + 11 + 13 + 999 + 700) / 6)
     assert P2.phase1(x, np.full(K, -1, np.int32), K, 1) is None
 
 
