@@ -241,12 +241,28 @@ class Workspace:
 def topk_host(scores: np.ndarray, ws: Workspace, k: int = MAX_K, row_lens: np.ndarray | None = None,
               prev: np.ndarray | None = None, out: np.ndarray | None = None, stream=None) -> np.ndarray:
     """End-to-end entry: HOST fp32 scores [R, stride] (pinned recommended) -> HOST int32
-    [R, k].  H2D copies, the GVR kernel and the D2H copy run inside the C call."""
-    if scores.dtype != np.float32 or scores.ndim != 2 or not scores.flags.c_contiguous:
+    [R, k].  H2D copies, the GVR kernel and the D2H copy run inside the C call.
+    row_lens [R] and prev [R, k] are converted to C-contiguous int32 when needed; out, if
+    given, must already be a C-contiguous int32 [R, k] array (it is written in place)."""
+    if not isinstance(scores, np.ndarray) or scores.dtype != np.float32 or scores.ndim != 2 \
+            or not scores.flags.c_contiguous:
         raise GvrError("scores must be a C-contiguous fp32 [R, stride] array")
     R, stride = scores.shape
+    if k != ws.k or stride != ws.row_stride or R > ws.max_rows:
+        raise GvrError(f"workspace holds up to {ws.max_rows} rows of stride {ws.row_stride}, k={ws.k}")
     if out is None:
         out = np.empty((R, k), dtype=np.int32)
+    elif not isinstance(out, np.ndarray) or out.dtype != np.int32 or out.shape != (R, k) \
+            or not out.flags.c_contiguous:
+        raise GvrError("out must be a C-contiguous int32 [R, k] array")
+    if row_lens is not None:
+        row_lens = np.ascontiguousarray(np.asarray(row_lens), dtype=np.int32)
+        if row_lens.shape != (R,):
+            raise GvrError("row_lens must have shape [R]")
+    if prev is not None:
+        prev = np.ascontiguousarray(np.asarray(prev), dtype=np.int32)
+        if prev.shape != (R, k):
+            raise GvrError("prev must have shape [R, k]")
     lp = None if row_lens is None else ctypes.c_void_p(row_lens.ctypes.data)
     pp = None if prev is None else ctypes.c_void_p(prev.ctypes.data)
     sp = ctypes.c_void_p(0) if stream is None else _stream_ptr(stream)

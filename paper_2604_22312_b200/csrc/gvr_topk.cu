@@ -61,34 +61,54 @@ cudaMemPool_t scratch_pool()
 
 // Per-(device, stream) scratch of the batch path, grown stream-ordered from scratch_pool()
 // and then reused: steady-state calls allocate nothing (CUDA-Graph friendly).  Calls on
-// one stream are serialised by the stream, so one buffer per stream is race-free.  While
-// the stream is being captured the cache is not modified: a too-small cache is bypassed
-// with an allocation / free pair recorded in the graph.
+// one stream are serialised by the stream, so one buffer per stream is race-free.
+//  * Slots are keyed by cudaStreamGetId, which is unique per stream — also for the
+//    per-thread default stream, whose handle value is the same on every host thread.
+//  * The lease holds the cache's lock until the caller has enqueued its kernels (the
+//    ScratchLease destructor), so no other host thread can grow the slot and free the
+//    buffer between the lookup and the launches.
+//  * A stream being captured never uses (or changes) the cache: the call takes a
+//    graph-owned allocation / free pair recorded in the graph, zeroed by a memset node,
+//    so every graph owns its scratch and a later eager call cannot free it under it.
+//  * A failed call leaves the slot marked dirty; the next lease clears its zero region.
 //
 // Layout: a zero region at fixed offsets — ctl[4] | qctl[4] | queue[rows_cap] |
 // segdone[rows_cap] — whose words are zero between calls (each kernel resets what it
 // used), sized by the lease's row capacity so that calls with fewer rows leave the tail
 // untouched; then the per-call arrays (zero_region_bytes(rows_cap) onwards).
+struct ScratchSlot {
+    void* ptr = nullptr;
+    size_t size = 0;
+    int64_t rows_cap = 0;
+    bool dirty = false;  // a call failed after taking the lease: re-zero before reuse
+};
+
 struct ScratchLease {
     unsigned char* ptr = nullptr;
     int64_t rows_cap = 0;
-    bool temporary = false;  // free after the launch (capture-time allocation)
-    bool fresh = false;      // newly allocated: its zero region must be cleared
+    bool temporary = false;         // free after the launch (capture-time allocation)
+    bool fresh = false;             // newly allocated or dirty: its zero region must be cleared
+    ScratchSlot* slot = nullptr;    // the cached slot (nullptr for a temporary)
+    std::unique_lock<std::mutex> lock;
+    void fail()
+    {
+        if (slot) slot->dirty = true;
+    }
 };
 
 size_t zero_region_bytes(int64_t rows_cap) { return (32 + 8 * (size_t)rows_cap + 255) & ~(size_t)255; }
+
+std::mutex& scratch_mutex()
+{
+    static std::mutex mu;
+    return mu;
+}
 
 // bytes_after(rows_cap): bytes needed past the zero region for this call
 template <class F>
 cudaError_t acquire_scratch(cudaStream_t stream, int64_t rows, F bytes_after, ScratchLease& lease)
 {
-    struct Slot {
-        void* ptr = nullptr;
-        size_t size = 0;
-        int64_t rows_cap = 0;
-    };
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, Slot> cache;
+    static std::map<std::pair<int, unsigned long long>, ScratchSlot> cache;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -96,21 +116,27 @@ cudaError_t acquire_scratch(cudaStream_t stream, int64_t rows, F bytes_after, Sc
     if (!pool) return cudaErrorMemoryAllocation;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if ((e = cudaStreamIsCapturing(stream, &cap)) != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lock(mu);
-    Slot& slot = cache[std::make_pair(dev, stream)];
+    if (cap != cudaStreamCaptureStatusNone) {
+        const size_t need = zero_region_bytes(rows) + bytes_after(rows);
+        lease.temporary = true;
+        lease.fresh = true;
+        lease.rows_cap = rows;
+        return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&lease.ptr), need, pool, stream);
+    }
+    unsigned long long sid = 0;
+    if ((e = cudaStreamGetId(stream, &sid)) != cudaSuccess) return e;
+    lease.lock = std::unique_lock<std::mutex>(scratch_mutex());
+    ScratchSlot& slot = cache[std::make_pair(dev, sid)];
+    lease.slot = &slot;
     if (slot.ptr && slot.rows_cap >= rows && slot.size >= zero_region_bytes(slot.rows_cap) + bytes_after(slot.rows_cap)) {
         lease.ptr = static_cast<unsigned char*>(slot.ptr);
         lease.rows_cap = slot.rows_cap;
+        lease.fresh = slot.dirty;
+        slot.dirty = false;
         return cudaSuccess;
     }
     const int64_t rc = rows > slot.rows_cap ? rows : slot.rows_cap;
     const size_t need = zero_region_bytes(rc) + bytes_after(rc);
-    if (cap != cudaStreamCaptureStatusNone) {
-        lease.temporary = true;
-        lease.fresh = true;
-        lease.rows_cap = rc;
-        return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&lease.ptr), need, pool, stream);
-    }
     const size_t grow = need > 2 * slot.size ? need : 2 * slot.size;
     void* p = nullptr;
     if ((e = cudaMallocFromPoolAsync(&p, grow, pool, stream)) != cudaSuccess) return e;
@@ -118,6 +144,7 @@ cudaError_t acquire_scratch(cudaStream_t stream, int64_t rows, F bytes_after, Sc
     slot.ptr = p;
     slot.size = grow;
     slot.rows_cap = rc;
+    slot.dirty = false;
     lease.ptr = static_cast<unsigned char*>(p);
     lease.rows_cap = rc;
     lease.fresh = true;
@@ -374,6 +401,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     if (lease.fresh && cudaMemsetAsync(scratch, 0, zero_region_bytes(lease.rows_cap), stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         if (lease.temporary) (void)cudaFreeAsync(scratch, stream);
+        lease.fail();
         return GVR_ERR_CUDA;
     }
     // programmatic dependent launch: each kernel is scheduled while its predecessor runs
@@ -423,6 +451,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     }
     mark(3);
     const gvr_status ls = e != cudaSuccess ? GVR_ERR_CUDA : launch_status();
+    if (ls != GVR_OK) lease.fail();  // kernels of this call may not have reset the zero region
     if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
         g_last_cuda_error = cudaGetLastError();
         return GVR_ERR_CUDA;

@@ -616,3 +616,66 @@ def test_filter_path_alternating_batch_sizes_and_paths(gvr):
                        prev=torch.from_numpy(prev).to(dev), options=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
         torch.cuda.synchronize()
         _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens)
+
+
+# ------------------------------------------------------------------ scratch lease
+def test_graph_captured_on_warm_stream_survives_eager_growth(gvr):
+    """Warm up and capture on the SAME stream (the cache already holds a big-enough slot),
+    then grow that stream's slot with a larger eager call, then replay: the graph owns its
+    own scratch, so the replay is exact."""
+    import torch
+    dev = torch.device("cuda:0")
+    host_a, lens, prev_a = _decode_rows(300, n=12_000, seed=1600)
+    host_big, lens_big, prev_big = _decode_rows(600, n=12_000, seed=1601)
+    s = torch.from_numpy(host_a).to(dev)
+    l = torch.from_numpy(lens).to(dev)
+    p = torch.from_numpy(prev_a).to(dev)
+    out = torch.empty((300, K), dtype=torch.int32, device=dev)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        gvr.topk(s, K, row_lens=l, prev=p, out=out)  # sizes the stream's slot
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            gvr.topk(s, K, row_lens=l, prev=p, out=out)
+        big = gvr.topk(torch.from_numpy(host_big).to(dev), K, row_lens=torch.from_numpy(lens_big).to(dev),
+                       prev=torch.from_numpy(prev_big).to(dev))  # grows (and frees) the slot
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.topk_batched(host_a, K, row_lens=lens))
+    assert np.array_equal(big.cpu().numpy(), oracle.topk_batched(host_big, K, row_lens=lens_big))
+
+
+def test_per_thread_default_streams_from_two_host_threads(gvr):
+    """Two host threads each call GVR on their own per-thread default stream (one handle
+    value, two streams): each keeps its own scratch lease."""
+    import threading
+
+    import torch
+    dev = torch.device("cuda:0")
+    jobs = [_decode_rows(300, n=9_000, seed=1700 + i) for i in range(2)]
+    results, errors = [None, None], []
+
+    def work(i):
+        try:
+            torch.cuda.set_device(dev)
+            host, lens, prev = jobs[i]
+            s = torch.from_numpy(host).to(dev)
+            l = torch.from_numpy(lens).to(dev)
+            p = torch.from_numpy(prev).to(dev)
+            ptd = torch.cuda.ExternalStream(2)  # cudaStreamPerThread
+            outs = [gvr.topk(s, K, row_lens=l, prev=p, stream=ptd) for _ in range(4)]
+            torch.cuda.synchronize()
+            results[i] = [o.cpu().numpy() for o in outs]
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for (host, lens, _), res in zip(jobs, results):
+        ref = oracle.topk_batched(host, K, row_lens=lens)
+        for o in res:
+            assert np.array_equal(o, ref)

@@ -97,3 +97,27 @@ def test_binding_fails_loudly_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(gvr.GvrError):
         gvr.topk(torch.zeros(2, 100), 8)
+
+
+def test_topk_host_validates_host_arrays():
+    """topk_host checks its host arrays before the C call: a wrong-dtype or
+    wrong-shape out is refused, row_lens / prev of another integer type are converted."""
+    import types
+
+    import numpy as np
+
+    import paper_2604_22312_b200 as gvr
+    ws = types.SimpleNamespace(k=2048, row_stride=16, max_rows=2, _h=None)
+    s = np.zeros((2, 16), np.float32)
+    with pytest.raises(gvr.GvrError):
+        gvr.topk_host(s, ws, 2048, out=np.zeros((2, 2048), np.int64))
+    with pytest.raises(gvr.GvrError):
+        gvr.topk_host(s, ws, 2048, out=np.zeros((2, 1024), np.int32))
+    with pytest.raises(gvr.GvrError):
+        gvr.topk_host(s, ws, 2048, row_lens=np.zeros(3, np.int64))
+    with pytest.raises(gvr.GvrError):
+        gvr.topk_host(s, ws, 2048, prev=np.zeros((2, 7), np.int32))
+    with pytest.raises(gvr.GvrError):
+        gvr.topk_host(np.zeros((3, 16), np.float32), ws, 2048)  # more rows than the workspace
+    with pytest.raises(gvr.GvrError):
+        gvr.topk_host(s.astype(np.float64), ws, 2048)
