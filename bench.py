@@ -10,14 +10,18 @@ scores (Eq. 1, synthetic, prev-step guesses), K = 2048.  Inputs are res
 in HBM before the timed region; three distinct batches are rotated so every step reads
 cold data (3 x 195 MB > 126 MB L2).  Rank 0 prints one JSON line.
 
-A step launches two kernels of ours (gvr_guess_kernel: Phase 1 for every row, then
-gvr_topk_kernel: stream + Phases 2-4 + ordered output); the roofline entry is for the
-dominant one (the streaming kernel), timed by CUDA events recorded on its stream through
-gvr_topk_batched_events in a separate pass after the timed region (every 4th call).
+A step of the default (batch filter) path launches four kernels of ours: gvr_guess_kernel
+(Phases 1-2 for every row), gvr_filter_kernel (the one HBM pass, candidate lists),
+gvr_refine_kernel (Phase 4 + ordered output per row) and gvr_fixup_kernel (rows the
+lists cannot finish; usually none).  The roofline entry is for the dominant one (the
+filter kernel), timed by CUDA events recorded on its stream through
+gvr_topk_batched_events in a separate pass after the timed region (every 4th call);
+roofline.whole_call is SURVEY 8(d)'s B(N) * R / elapsed over the whole call.
 
-Under torchrun (N > 1) every rank processes its own batch of the same shape (rows are
-independent; no collective on the hot path) — weak scaling; the elapsed time is the
-max over ranks.  cfg5 instead splits one fixed 64 x 61 batch across the ranks
+--gpus N > 1 without WORLD_SIZE re-runs this command under torch.distributed.run (one
+rank per GPU, 127.0.0.1).  Under torchrun every rank processes its own batch of the same
+shape (rows are independent; no collective on the hot path) — weak scaling; the elapsed
+time is the max over ranks.  cfg5 instead splits one fixed 64 x 61 batch across the ranks
 (paper_2604_22312_b200.shard.row_partition) — strong scaling.  --gather also times the
 optional NCCL all-gather of out_idx, reported separately.  --impl reference times the
 CPU oracle on the host (rank 0 only).
@@ -243,6 +247,16 @@ def time_steps(fn, batches, steps, warmup, stream, sampler=None, kernel_events=F
     return total, {"guess": mean(0, 1), "stream": mean(1, 2), "refine": mean(2, 3), "sampled_steps": len(evs)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_oracle_rate(host_scores, lens, max_rows=None, threads=None):
     import oracle
     rows = host_scores if max_rows is None else host_scores[:max_rows]
@@ -270,10 +284,15 @@ def main():
                     help="batch path of the library (gvr_options.batch_path): filter kernel + refine, or row kernel")
     ap.add_argument("--gather", action="store_true",
                     help="N > 1: also time the optional NCCL all-gather of out_idx (reported separately)")
+    ap.add_argument("--cpu-dry-run", action="store_true",
+                    help="launcher / rank-plumbing check without a GPU: gloo process group, no kernels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run this command under torch.distributed.run (rank 0 prints)
+        return launch_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -281,6 +300,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
+    if args.cpu_dry_run:
+        return run_dry(args, cfg, rank, world)
 
     import torch
     import __graft_entry__
@@ -436,7 +457,11 @@ def main():
         peak = float(peaks.get("hbm_gbs", 6650.0))
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
         abytes = algorithmic_bytes(lens_np)
-        if fused:
+        G = int(st[:, 7].max()) if args.impl == "gvr" else 1  # CTAs per row (stats.cluster)
+        if fused and G > 1:
+            stream_kernel, n_kernels = "gvr_topk_cluster_kernel", 1
+            gvr_path = f"cluster kernel: {G} CTAs per row merged through DSMEM (few long rows)"
+        elif fused:
             stream_kernel, n_kernels, gvr_path = "gvr_topk_kernel", 1, "fused single kernel (one wave)"
         elif args.path == "filter":
             stream_kernel, n_kernels = "gvr_filter_kernel", 4  # guess, filter, refine, fixup
@@ -447,7 +472,8 @@ def main():
 
         def kernel_us(kt):
             names = {"guess": "gvr_guess_kernel", "stream": stream_kernel,
-                     "refine": "gvr_topk_kernel (refine)" if stream_kernel == "gvr_filter_kernel" else None}
+                     "refine": "gvr_refine_kernel + gvr_fixup_kernel" if stream_kernel == "gvr_filter_kernel"
+                     else None}
             d = {names[k]: round(kt[k] * 1e6, 2) for k in ("guess", "stream", "refine") if names[k]}
             return d | {"sampled_steps": kt["sampled_steps"]}
         step_gbs = abytes / (elapsed / args.steps) / 1e9  # whole call (all kernels + gaps)
@@ -497,7 +523,10 @@ def main():
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes,
                          "kernel": stream_kernel if args.impl == "gvr" else "radix_topk_kernel",
                          "kernel_us_per_launch": round(kern_s * 1e6, 2),
-                         "step_gbs": round(step_gbs, 1)},
+                         "step_gbs": round(step_gbs, 1),
+                         # SURVEY 8(d)'s definition over the whole call: B(N) * R / elapsed
+                         "whole_call": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak, 4),
+                                        "algorithmic_bytes_per_call": abytes}},
             "kernel_us_per_launch": (kernel_us(kern_times) if kern_times else None),
             "passes_per_row": {"global_mean": float(st[:, 4].mean()), "secant_mean": float(st[:, 0].mean()),
                                "snap_mean": float(st[:, 1].mean()), "raises_mean": float(st[:, 5].mean()),
@@ -514,12 +543,74 @@ def main():
     if rank == 0 and not args.no_cpu:
         host0 = batches[0]["scores"].cpu().numpy()
         rate, threads, nrows, dt = cpu_oracle_rate(host0, lens_np)
+        n1 = min(8, nrows)
+        rate1, _, _, dt1 = cpu_oracle_rate(host0, lens_np, max_rows=n1, threads=1)
         result["cpu_baseline"] = {"value": round(rate, 2), "unit": "rows/s", "cores": threads, "kind": "oracle",
                                   "sample": f"{nrows} rows of {args.config} (one full batch), qsort oracle, "
-                                            f"{dt:.2f} s wall on {threads} threads"}
+                                            f"{dt:.2f} s wall on {threads} threads",
+                                  "single_thread_ms_per_row": round(dt1 / n1 * 1e3, 3),
+                                  "cpu_model": cpu_model()}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def launch_ranks(n):
+    """`bench.py --gpus N` without WORLD_SIZE: start N ranks on this node with
+    torch.distributed.run (rendezvous on 127.0.0.1, a free port) and wait for them."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+
+
+def run_dry(args, cfg, rank, world):
+    """--cpu-dry-run: the multi-rank plumbing of the real run (process group, barrier +
+    max-over-ranks timing, aggregate rows/s, rank-0 JSON line) on gloo without kernels; the
+    per-rank work is the config's row partition with a host-side stand-in step."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    split = bool(cfg.get("split"))
+    from paper_2604_22312_b200.shard import row_partition
+    per_req = cfg["layers"] * cfg["draft"]
+    if split:  # strong scaling: contiguous blocks of requests, as in the real run
+        qb = row_partition(np.full(cfg["requests"], cfg["n"]), world)
+        R = int(qb[rank + 1] - qb[rank]) * per_req
+    else:
+        R = cfg["requests"] * per_req
+    x = np.random.default_rng(rank).standard_normal((min(R, 8), 4096)).astype(np.float32)
+    for _ in range(args.warmup):
+        np.sort(x, axis=1)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        np.sort(x, axis=1)
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+        n = torch.tensor([R], dtype=torch.int64)
+        dist.all_reduce(n)
+        rows_all = int(n.item())
+    else:
+        rows_all = R
+    if rank == 0:
+        print(json.dumps({"metric": "dry run (no kernels)", "value": round(rows_all * args.steps / el, 1),
+                          "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "scaling": "strong" if split else "weak", "rows_per_rank0": R, "rows_all": rows_all,
+                          "config": {"workload": args.config}}), flush=True)
+    if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -88,3 +88,27 @@ def test_world2_shard_and_gather_matches_unsharded(tmp_path):
     host, lens = _batch()
     ref = oracle.topk_batched(host, K, row_lens=lens)
     assert np.array_equal(np.load(out), ref)
+
+
+@pytest.mark.parametrize("config", ["cfg2", "cfg5"])
+def test_bench_launcher_starts_the_ranks(config):
+    """`bench.py --gpus 2` without WORLD_SIZE starts two ranks itself (torch.distributed.run
+    on 127.0.0.1); rank 0 prints one JSON line with n_gpus = 2 and the max-over-ranks
+    aggregate (the --cpu-dry-run mode runs the rank plumbing on gloo without kernels)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--cpu-dry-run",
+                          "--steps", "2", "--warmup", "3", "--config", config],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2
+    if config == "cfg5":  # strong scaling: 64 requests x 61 layers split in halves
+        assert d["scaling"] == "strong" and d["rows_all"] == 3904 and d["rows_per_rank0"] == 1952
+    else:
+        assert d["scaling"] == "weak" and d["rows_all"] == 2 * 488
