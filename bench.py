@@ -275,7 +275,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--impl", default="gvr", choices=["gvr", "radix", "reference"])
+    ap.add_argument("--impl", default="gvr", choices=["gvr", "radix", "radix2", "reference"])
     ap.add_argument("--nbatches", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -350,7 +350,10 @@ def main():
     def radix_step(b):
         gvr.radix_topk(b["scores"], K, row_lens=b["row_lens"], out=b["out"])
 
-    main_fn = gvr_step if args.impl == "gvr" else radix_step
+    def radix2_step(b):
+        gvr.radix2_topk(b["scores"], K, row_lens=b["row_lens"], out=b["out"])
+
+    main_fn = {"gvr": gvr_step, "radix": radix_step, "radix2": radix2_step}[args.impl]
     other_fn = radix_step if args.impl == "gvr" else gvr_step
 
     # correctness gate (oracle) on one batch before timing
@@ -410,12 +413,16 @@ def main():
     rows_total = rows_all * args.steps
     value = rows_total / elapsed
 
-    # the other kernel, same protocol (speedup vs own radix select)
+    # the other kernel, same protocol (speedup vs own radix select), and the same-geometry
+    # radix baseline (radix2: histogram pass + the GVR filter / refine machinery)
     other_elapsed = time_steps(other_fn, batches, args.steps, args.warmup, stream, flush=flush)
+    r2_elapsed = (time_steps(radix2_step, batches, args.steps, args.warmup, stream, flush=flush)
+                  if args.impl == "gvr" else None)
     if dist is not None:
-        t = torch.tensor([other_elapsed], device=dev)
+        t = torch.tensor([other_elapsed, r2_elapsed or 0.0], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        other_elapsed = float(t.item())
+        other_elapsed = float(t[0].item())
+        r2_elapsed = float(t[1].item()) if r2_elapsed is not None else None
 
     # optional all-gather of every rank's indices (off the hot path, timed separately)
     gather_info = None
@@ -443,6 +450,8 @@ def main():
     b0 = batches[0]
     if args.impl == "gvr":
         _, _, st = gvr.topk_ex(b0["scores"], K, row_lens=b0["row_lens"], prev=b0["prev"], values=False)
+    elif args.impl == "radix2":
+        _, _, st = gvr.radix2_topk_ex(b0["scores"], K, row_lens=b0["row_lens"], values=False)
     else:
         _, _, st = gvr.radix_topk_ex(b0["scores"], K, row_lens=b0["row_lens"], values=False)
     st = st.cpu().numpy()
@@ -517,11 +526,19 @@ def main():
             "us_per_row": round(elapsed / (R * args.steps) * 1e6, 5),
             "speedup_vs_radix": round(rad_t / gvr_t, 3),
             "radix_rows_per_s": round(rows_all * args.steps / rad_t, 1),
+            # the same-geometry radix (radix2_topk_batched: one half-digit histogram pass +
+            # the GVR filter / refine machinery): the fair comparison
+            "speedup_vs_radix_same_geometry": (round(r2_elapsed / gvr_t, 3) if r2_elapsed else None),
+            "radix2_rows_per_s": (round(rows_all * args.steps / r2_elapsed, 1) if r2_elapsed else None),
+            "radix_baselines": {"radix": "radix_topk_batched: one CTA per row, 11/11/10-bit rounds re-reading "
+                                         "the row, early exit (PAPER.md:125-148)",
+                                "radix2": "radix2_topk_batched: persistent TMA stream of the half digit "
+                                          "histogram, then the GVR filter at the K-th bin and the GVR refine"},
             "hbm_gbs": round(step_gbs, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes,
-                         "kernel": stream_kernel if args.impl == "gvr" else "radix_topk_kernel",
+                         "kernel": stream_kernel if args.impl == "gvr" else f"{args.impl}_topk (whole call)",
                          "kernel_us_per_launch": round(kern_s * 1e6, 2),
                          "step_gbs": round(step_gbs, 1),
                          # SURVEY 8(d)'s definition over the whole call: B(N) * R / elapsed
@@ -531,7 +548,7 @@ def main():
             "passes_per_row": {"global_mean": float(st[:, 4].mean()), "secant_mean": float(st[:, 0].mean()),
                                "snap_mean": float(st[:, 1].mean()), "raises_mean": float(st[:, 5].mean()),
                                "cand_mean": float(st[:, 2].mean())},
-            "gpu_launches": args.steps * (n_kernels if args.impl == "gvr" else 1),
+            "gpu_launches": args.steps * (n_kernels if args.impl == "gvr" else (5 if args.impl == "radix2" else 1)),
             "gvr_path": gvr_path if args.impl == "gvr" else None,
             "clocks": clk.summary(),
             "allgather": gather_info,

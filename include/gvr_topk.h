@@ -166,6 +166,22 @@ gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const 
                                  int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream,
                                  float* out_val, gvr_row_stats* stats);
 
+/* Same-geometry radix baseline: the radix select run on
+ * the machinery of the GVR batch path ("identical thread-level
+ * resources").  Pass 1 streams the whole batch once (persistent CTAs, TMA ring; long rows
+ * split over several CTAs) into a 2048-bin histogram per row of the
+ * paper's 16-bit "half" digit (top 11 bits of the fp16-rounded score's sortable key,
+ * PAPER.md:138, 143-147); the K-th bin gives a collect threshold T1; pass 2 is the GVR
+ * filter kernel at T1 and the GVR refine / fixup kernels finish the remaining digits on
+ * the candidate lists.  Same output contract and scratch conventions as gvr_topk_batched
+ * (no guess); two HBM passes per row. */
+gvr_status radix2_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                               int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream);
+
+gvr_status radix2_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                                  int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                                  float* out_val, gvr_row_stats* stats);
+
 /* ---- host-buffer entry point (end-to-end use) ------------------------------------
  * A workspace owns device buffers for up to max_rows rows of row_stride elements and
  * k outputs.  gvr_topk_batched_host copies HOST scores/row_lens/prev (pinned memory

@@ -7,6 +7,7 @@ PyTorch fallback — if the library or a CUDA device is missing, calls raise.
 
     topk(scores, k=2048, row_lens=None, prev=None)   -> int32 [R, k] (GVR)
     radix_topk(scores, k=2048, row_lens=None)         -> int32 [R, k] (radix baseline)
+    radix2_topk(scores, k=2048, row_lens=None)        -> int32 [R, k] (same-geometry radix)
     topk_ex(...)                                      -> (idx, values, stats)
     topk_host(scores_np, ...)                         -> host-buffer C-ABI entry point
 
@@ -56,6 +57,8 @@ def _load():
         "gvr_topk_batched_ex": [vp, i64, vp, i32, vp, i32, vp, vp, vp, vp, vp],
         "radix_topk_batched": [vp, i64, vp, i32, i32, vp, vp],
         "radix_topk_batched_ex": [vp, i64, vp, i32, i32, vp, vp, vp, vp],
+        "radix2_topk_batched": [vp, i64, vp, i32, i32, vp, vp],
+        "radix2_topk_batched_ex": [vp, i64, vp, i32, i32, vp, vp, vp, vp],
         "gvr_workspace_create": [i32, i64, i32, ctypes.POINTER(vp)],
         "gvr_workspace_destroy": [vp],
         "gvr_topk_batched_host": [vp, i64, vp, i32, vp, i32, vp, vp, vp],
@@ -215,6 +218,23 @@ def radix_topk_ex(scores, k: int = MAX_K, row_lens=None, out=None, values=True, 
     st = torch.zeros((R, len(STATS_FIELDS)), dtype=torch.int32, device=scores.device) if stats else None
     _check(_load().radix_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, k, _ptr(out),
                                          _stream_ptr(stream), _ptr(val), _ptr(st)))
+    return out, val, st
+
+
+def radix2_topk(scores, k: int = MAX_K, row_lens=None, out=None, stream=None):
+    """Same-geometry radix baseline (histogram pass + GVR filter / refine machinery)."""
+    R, stride, row_lens, _, out = _prep(scores, k, row_lens, None, out)
+    _check(_load().radix2_topk_batched(_ptr(scores), stride, _ptr(row_lens), R, k, _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def radix2_topk_ex(scores, k: int = MAX_K, row_lens=None, out=None, values=True, stats=True, stream=None):
+    torch = _torch()
+    R, stride, row_lens, _, out = _prep(scores, k, row_lens, None, out)
+    val = torch.empty((R, k), dtype=torch.float32, device=scores.device) if values else None
+    st = torch.zeros((R, len(STATS_FIELDS)), dtype=torch.int32, device=scores.device) if stats else None
+    _check(_load().radix2_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, k, _ptr(out),
+                                          _stream_ptr(stream), _ptr(val), _ptr(st)))
     return out, val, st
 
 

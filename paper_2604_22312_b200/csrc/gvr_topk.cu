@@ -10,6 +10,7 @@
 #include "gvr_kernel.cuh"
 #include "refine_kernel.cuh"
 #include "radix_kernel.cuh"
+#include "radix2_kernel.cuh"
 
 namespace {
 
@@ -245,10 +246,13 @@ gvr_status gvr_kernel_info(int32_t* gvr_ctas_per_sm, int32_t* gvr_threads, int32
 
 const char* gvr_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 
+// radix2: the same-geometry radix baseline (radix2_kernel.cuh) — the batch filter path
+// with its Phase 1-2 guess kernel replaced by a histogram pass over the batch and a
+// per-row threshold kernel; used for every batch size.
 static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
                              const int32_t* prev_topk, int32_t k, int32_t* out_idx, cudaStream_t stream,
                              const gvr_options* opt, float* out_val, gvr_row_stats* stats, long long* phase_ts,
-                             cudaEvent_t const* ev = nullptr)
+                             cudaEvent_t const* ev = nullptr, bool radix2 = false)
 {
     gvr_status st = validate(scores, row_stride, num_rows, k, out_idx);
     if (st != GVR_OK) return st;
@@ -277,8 +281,10 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     // rows long — G = the largest power of two <= 8 with >= 16K elements per slice and
     // num_rows * G within one wave; gvr_options.force_cluster (1, 2, 4, 8) overrides.
     int G = 1;
-    const int wave = fused_max_rows();
-    if (opt && opt->force_cluster > 0) {
+    const int wave = radix2 ? 0 : fused_max_rows();
+    if (radix2) {
+        G = 1;
+    } else if (opt && opt->force_cluster > 0) {
         G = opt->force_cluster;
         if (G != 1 && G != 2 && G != 4 && G != 8) return GVR_ERR_UNSUPPORTED;
     } else {
@@ -312,7 +318,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         }
         return launch_status();
     }
-    if (num_rows <= wave) {
+    if (num_rows <= wave && !radix2) {
         // one wave: a single launch, Phase 1 inside each row's CTA (no hand-off, no
         // scratch); the gathers overlap the CTA's first tile loads
         mark(0);
@@ -337,7 +343,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     // stream's cached lease (acquire_scratch).
     CandLists cl{};
     BatchQueue bq{};
-    bool filt = !(opt && opt->batch_path == 1);
+    bool filt = radix2 || !(opt && opt->batch_path == 1);
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess || sms < 1) {
         int dev = 0;
@@ -349,13 +355,13 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         }
     }
     // per-call arrays after the zero region: GuessOut[R] | order[R] | fixlist[R] |
-    // rec[R][F_SEGS] | region[G][reg]
+    // rec[R][F_SEGS] | [radix2: hist[R][NBINS]] | region[G][reg]
     const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
     const size_t order_off = gp_bytes;
     const size_t fix_off = order_off + (size_t)num_rows * 4;
     const size_t rec_off = (fix_off + (size_t)num_rows * 4 + 255) & ~(size_t)255;
     size_t after_bytes = fix_off;
-    size_t region_off = 0;
+    size_t region_off = 0, hist_off = 0;
     if (filt) {
         const int tpr = (int)((row_stride + STAGE_FLOATS - 1) / STAGE_FLOATS);
         const long long V = (long long)num_rows * tpr;
@@ -366,16 +372,19 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         long long reg = per * STAGE_FLOATS / 8;  // room for 1/8 of the elements
         if (reg < F_REG_MIN) reg = F_REG_MIN;
         if (G < 1 || G * reg > 0x7fffffffLL) {
+            if (radix2) return GVR_ERR_UNSUPPORTED;
             filt = false;
         } else {
             cl.V = V;
             cl.G = (int)G;
             cl.tpr = tpr;
             cl.reg = (int)reg;
-            region_off = (rec_off + (size_t)num_rows * F_SEGS * sizeof(int4) + 255) & ~(size_t)255;
+            hist_off = (rec_off + (size_t)num_rows * F_SEGS * sizeof(int4) + 255) & ~(size_t)255;
+            region_off = hist_off + (radix2 ? (size_t)num_rows * NBINS * sizeof(uint32_t) : 0);
             after_bytes = region_off + (size_t)G * (size_t)reg * sizeof(uint2);
         }
     }
+    if (radix2 && (st = set_smem(radix_hist_kernel, RH_SMEM_BYTES)) != GVR_OK) return st;
     if (filt && ((st = set_smem(gvr_filter_kernel, F_SMEM_BYTES)) != GVR_OK ||
                  (st = set_smem(gvr_refine_kernel, RF_SMEM_BYTES)) != GVR_OK ||
                  (st = set_smem(gvr_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK))
@@ -424,8 +433,26 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     };
     cudaError_t e = cudaSuccess;
     mark(0);
-    gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm, gp,
-                                                        sched, bq);
+    if (radix2) {
+        uint32_t* ghist = reinterpret_cast<uint32_t*>(per_call + hist_off);
+        e = cudaMemsetAsync(ghist, 0, (size_t)num_rows * NBINS * sizeof(uint32_t), stream);
+        if (e == cudaSuccess)
+            e = launch(radix_hist_kernel, cl.G, RH_NT, RH_SMEM_BYTES, scores, row_stride, row_lens, (int)k, cl,
+                       ghist);
+        const uint32_t* ghc = ghist;
+        if (e == cudaSuccess)
+            e = launch(radix_thresh_kernel, (int)num_rows, 256, 0, scores, row_stride, row_lens, (int)k, ghc, gp, bq);
+        if (e != cudaSuccess) {
+            g_last_cuda_error = e;
+            (void)cudaGetLastError();
+            lease.fail();
+            if (lease.temporary) (void)cudaFreeAsync(scratch, stream);
+            return GVR_ERR_CUDA;
+        }
+    } else {
+        gvr_guess_kernel<<<num_rows, GUESS_NT, 0, stream>>>(scores, row_stride, row_lens, prev_topk, k, num_rows, prm,
+                                                            gp, sched, bq);
+    }
     mark(1);
     const GuessOut* gpc = gp;
     const int32_t* orderc = sched.order;
@@ -504,6 +531,20 @@ gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const 
     radix_topk_kernel<<<num_rows, RADIX_NT, RADIX_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
                                                             stats);
     return launch_status();
+}
+
+gvr_status radix2_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens,
+                                  int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream,
+                                  float* out_val, gvr_row_stats* stats)
+{
+    return gvr_launch(scores, row_stride, row_lens, num_rows, nullptr, k, out_idx, stream, nullptr, out_val, stats,
+                      nullptr, nullptr, true);
+}
+
+gvr_status radix2_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
+                               int32_t k, int32_t* out_idx, cudaStream_t stream)
+{
+    return radix2_topk_batched_ex(scores, row_stride, row_lens, num_rows, k, out_idx, stream, nullptr, nullptr);
 }
 
 gvr_status radix_topk_batched(const float* scores, int64_t row_stride, const int32_t* row_lens, int32_t num_rows,
