@@ -160,9 +160,9 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
     bisection after MAX_SECANT steps or when the bracket is too narrow for a float
     point).  Before the first secant step it probes T0 = pmean and then the Phase-1
     bracket end on the far side of the window.  Exits: DONE_WINDOW (T_c = T), DONE_TIES
-    (adjacent anchors: no key in the window — ties), DONE_EXHAUSTED (MAX_ITERS probes) —
-    the last two take T_c = the lo anchor, whose count is above the window (the safe
-    side).
+    (adjacent anchors: no key in the window — a tie group spans it; T_c = the lo anchor,
+    whose count is above the window), DONE_EXHAUSTED (MAX_ITERS probes; T_c = the sample
+    key of rank ceil(f_t), the exact finisher over the sample).
     Returns (T_c key, I = probes, done, count at T_c)."""
     L, H, ft = window(n, k, z)
     sk = np.asarray(sample_keys, dtype=np.uint32)
@@ -202,7 +202,10 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
         if khi - klo < 2:
             return klo, it, DONE_TIES, clo
         if it >= MAX_ITERS:
-            return klo, it, DONE_EXHAUSTED, clo
+            # the exact finisher over the sample (R12): the key of rank ceil(f_t)
+            rank = (L + H + 1) // 2
+            T = int(np.sort(sk)[::-1][rank - 1])
+            return T, it, DONE_EXHAUSTED, int(np.count_nonzero(sk >= np.uint32(T)))
         T = secant_step(klo, clo, khi, chi, ft, first_secant, secants >= max_secant)
         first_secant = False
         secants += 1
@@ -211,7 +214,8 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
             return T, it, DONE_WINDOW, r
 
 
-def replay_row(x: np.ndarray, guess, k: int, head: int = 0, stride: int = 8, z=Z, max_secant: int = MAX_SECANT):
+def replay_row(x: np.ndarray, guess, k: int, head: int = 0, stride: int = 8, z=Z, max_secant: int = MAX_SECANT,
+               filter_path: bool = False):
     """Phases 1-2 of one row as the guess kernel runs them (head: the row's scalars before
     its first 16-byte boundary; stride: the guess stride, used for n >= 32 k).  Returns a
     dict with the collect threshold key Tc, I, done (Phase-2 exit), window (L, H), the
@@ -230,4 +234,7 @@ def replay_row(x: np.ndarray, guess, k: int, head: int = 0, stride: int = 8, z=Z
         p1 = (int(sk.min()), int(sk.max()), f32(tree_sum(sv.reshape(SAMPLE_CHUNKS, CHUNK)) / f32(S)), S)
     Tc, it, done, c = phase2(sk, p1, n, k, z, max_secant)
     L, H, _ = window(n, k, z)
-    return dict(Tc=Tc, I=it, done=done, L=L, H=H, count=c, p1=p1)
+    tie = Tc if done == DONE_TIES else 0
+    if filter_path and done == DONE_TIES and Tc < 0xFFFFFFFF:
+        Tc += 1  # the batch filter path collects strictly above the tied key (R37)
+    return dict(Tc=Tc, I=it, done=done, L=L, H=H, count=c, p1=p1, tie=tie)

@@ -88,7 +88,7 @@ __device__ __forceinline__ long long sm_id()
 // What Phases 1-2 (phase12) hand to the streaming step, per row (32 bytes).
 struct GuessOut {
     uint32_t Tc;     // collect threshold key (Phase 2 result)
-    uint32_t pad;
+    uint32_t tie;    // Phase-2 ties exit: the tied sample key (the lo anchor), else 0
     uint32_t tmin;   // second-pass threshold: pmin when all k guesses were gathered and
                      // valid (then f(pmin) >= k for distinct guesses), else 0 (everything)
     uint32_t top;    // max(pmax, sample max) key
@@ -633,15 +633,48 @@ constexpr float P2_Z_DEFAULT = 4.5f;
 //     pmax (above), then Eq. 6 steps (secant_step) — a probe with L <= hits <= H ends
 //     the search.  Adjacent anchors (ties) or P2_MAX_ITERS probes -> the lo anchor, whose
 //     hits are above the window.
+// The rank-th largest of the group's 16 register keys per thread (1 <= rank <= 4096):
+// most-significant-digit radix select, 8 bits per level over a 256-bin shared histogram
+// (sh: 256 ints of the caller's shared memory).
 template <class G>
-__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm)
+__device__ __forceinline__ uint32_t sample_rank_key16(G& c, const uint32_t (&sk)[16], int32_t* sh, uint32_t rank)
+{
+    uint32_t prefix = 0u, pmask = 0u, rem = rank;
+    for (int level = 0; level < 4; ++level) {
+        const int shift = 24 - 8 * level;
+        sh[c.tid] = 0;
+        c.sync();
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if ((sk[q] & pmask) == prefix) atomicAdd(&sh[(sk[q] >> shift) & 255u], 1);
+        c.sync();
+        const int bin = 255 - c.tid;  // thread t owns bin 255 - t: descending digit order
+        const uint32_t h = (uint32_t)sh[bin];
+        uint32_t tot;
+        const uint32_t ex = group_excl_scan(c, h, tot);
+        if (ex < rem && ex + h >= rem) {
+            c.misc[0] = bin;
+            c.misc[1] = (int)ex;
+        }
+        c.sync();
+        prefix |= (uint32_t)c.misc[0] << shift;
+        pmask |= 255u << shift;
+        rem -= (uint32_t)c.misc[1];
+        c.sync();
+    }
+    return prefix;
+}
+
+template <class G>
+__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm,
+                                            int32_t* sh256)
 {
     static_assert(G::N == 256, "one sample chunk per thread");
     constexpr int GPT = KMAX / G::N;  // 8 guessed positions per thread
     GuessOut g;
-    g.pad = 0u;
     if (p.n <= GVR_CAP) {  // the whole row fits in B: collect everything, no search
         g.Tc = 0u;
+        g.tie = 0u;
         g.T0 = 0u;
         g.tmin = 0u;
         g.top = 0xffffffffu;
@@ -779,16 +812,27 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
         T = secant_step(klo, clo, khi, chi, ft, secants == 0, secants >= prm.max_secant);
         found = probe(T);
     }
-    if (!found) {
+    g.tie = 0u;
+    if (!found && exitk == GVR_P2_EXHAUSTED) {
+        // no probe landed in the window: the exact finisher over the sample (R12) — the
+        // sample key of rank ceil(f_t), whose hits are at least that rank
+        T = sample_rank_key16(c, sk, sh256, (uint32_t)((L + H + 1) / 2));
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < P2_CHUNK; ++q) m += sk[q] >= T ? 1u : 0u;
+        hits = group_red1<R_ADD>(c, m);
+    } else if (!found) {
+        // ties: the anchors are adjacent keys — the lo anchor's key holds a tie group that
+        // spans the window (its hits are above it, the next key's below)
         T = klo;
         hits = clo;
+        g.tie = klo;
     }
     g.Tc = T;
     g.T0 = f2key(pmean);
     g.t0_ok = isfinite(pmean) ? 1 : 0;
     g.tmin = (complete && kmn < T) ? kmn : 0u;
     g.top = max(kmx, smax);
-    g.pad = 0u;
     g.iters = (int16_t)it;
     g.exit = (int16_t)exitk;
     g.scount = (int32_t)hits;
@@ -829,7 +873,11 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
         if (c.tid == 0 && !bq.queue) sched.order[num_rows - 1 - atomicAdd(sched.cursors + 1, 1)] = r;
         return;
     }
-    const GuessOut g = phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm);
+    __shared__ int32_t sh[256];
+    GuessOut g = phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm, sh);
+    // filter path, a ties exit: collect the keys strictly above the tie; when they are
+    // fewer than K the refine kernel fills the rest with the tie's lowest indices (R37)
+    if (bq.queue && g.exit == GVR_P2_TIES && g.tie < 0xffffffffu) g.Tc = g.tie + 1u;
     if (c.tid == 0) {
         gp[r] = g;
         if (!bq.queue) {
@@ -900,7 +948,8 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
         st[2] = p.n;
     } else {
         // ---------------- Phases 1-2: in gvr_guess_kernel (batch paths) or here (fused)
-        gq = gp ? gp[r] : phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm);
+        gq = gp ? gp[r] : phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm,
+                                  reinterpret_cast<int32_t*>(smem + G_OFF_RHIST));
         RowMeta m;
         m.Tc = short_known ? gq.tmin : gq.Tc;
         if (short_known) passes = 2;
@@ -1034,7 +1083,7 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
 // streamed and refined in full — CTA b takes fixup-list entries b, b + G, ...  One CTA per
 // SM (the loop needs more registers than the row kernel's two-per-SM budget); the list is
 // usually empty.  The last CTA resets the batch queue's control words.
-__global__ void __launch_bounds__(GVR_NT, 1)
+__global__ void __launch_bounds__(GVR_NT, 2)
 gvr_fixup_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                  int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
                  const int32_t* prev, long long* phase_ts, int32_t* ctl, BatchQueue bq)
@@ -1194,7 +1243,7 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
         st[2] = pw.n;
     } else {
         // ---------------- Phase 1 (every CTA, identical result) and the slice stream
-        gq = phase12(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm);
+        gq = phase12(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm, rhist);
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         uint32_t Tc = gq.Tc, kmax = 0u, extras = 0u, Tm = 0u, kmx = 0u, T = 0u, tot = 0, pre = 0;
         int fill = 0, raises_all = 0;

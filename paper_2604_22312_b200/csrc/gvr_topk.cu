@@ -155,9 +155,8 @@ cudaError_t acquire_scratch(cudaStream_t stream, int64_t rows, F bytes_after, Sc
 // Largest batch handled by the single-launch fused path: one wave of the streaming
 // kernel (resident CTAs per SM x SMs), where the guess kernel's row ordering cannot help
 // and its extra launch and hand-off only add latency.
-// gvr_fixup_kernel's grid: the fixup list is usually empty, and a launch of many
-// 115 KB / 254-register CTAs costs microseconds even when they exit at once.
-constexpr int FIXUP_CTAS = 16;
+// gvr_fixup_kernel's grid: two CTAs per SM (the list is usually empty and every CTA then
+// exits at once; a batch of massive ties fills it).
 
 int fused_max_rows()
 {
@@ -465,7 +464,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
                        row_stride, row_lens, (int)k,
                        (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts);
         if (e == cudaSuccess)
-            e = launch(gvr_fixup_kernel, min((int)num_rows, FIXUP_CTAS), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
+            e = launch(gvr_fixup_kernel, min((int)num_rows, 2 * sms), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
                        (int)k, out_idx, out_val, stats, prm, gpc, prev_topk, phase_ts, ctl, bq);
     } else {
         e = launch(gvr_topk_kernel, (int)num_rows, GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens, (int)k, out_idx,

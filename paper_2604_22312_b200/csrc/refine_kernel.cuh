@@ -117,7 +117,10 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         // slots past the row's segment count are stale and ignored)
         const int4 erec = c.warp == 0 && c.lane < F_SEGS ? __ldcg(cl.rec + (long long)r * F_SEGS + c.lane)
                                                          : make_int4(0, 0, 0, 0);
-        uint32_t Tc = __ldcg(&gp[r].Tc);
+        const uint4 g0 = __ldcg(reinterpret_cast<const uint4*>(gp + r));      // Tc, tie, tmin, top
+        const uint4 g1 = __ldcg(reinterpret_cast<const uint4*>(gp + r) + 1);  // T0, iters | exit, ...
+        uint32_t Tc = g0.x;
+        const uint32_t tie = g0.y;
         const RowPlan p = plan_row(scores, stride, row_lens, r, k);
         // ---- the row's list segments (filter records)
         int total = -1;
@@ -162,11 +165,18 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             }
         }
         bool ok = p.ntiles > 0 && p.n > k && total >= K && total <= RF_MAXLIST && kmax >= Tc;
+        // a Phase-2 ties exit collected the keys strictly above the tied key (R37): when
+        // they are fewer than K, all of them lead the output and the tie's lowest indices
+        // follow (an ordered scan of the row below)
+        const int p2exit = (int)(int16_t)(g1.y >> 16);
+        const bool tie_fill = p.ntiles > 0 && p.n > k && p2exit == GVR_P2_TIES && tie < 0xffffffffu &&
+                              Tc == tie + 1u && total >= 0 && total < K;
+        if (tie_fill) ok = total == 0 || kmax >= Tc;
         // a row with len <= k: every element is selected (take = len), binned over its own
         // key range [min, max], then -1 padding (R5)
         const bool trivial = p.n <= k;
         const float* rowx = nullptr;
-        int take = K;
+        int take = tie_fill ? total : K;
         if (trivial) {
             uint32_t mn = 0xffffffffu, mx2 = 0u;
             for (int q = c.tid; q < p.n; q += RF_NT) {
@@ -188,7 +198,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         }
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         int ftc = 0, nsel = 0, levels = 0;
-        if (ok) {
+        if (ok && take > 0) {
             // ---- Phase 4: histogram of the keys >= lo over [lo, kmax],
             // the K-th bin from the bin scan.  lo starts at T_c; if the
             // bins up to the K-th one are too crowded to rank (keys spread over a wide key
@@ -309,11 +319,40 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                         if (ov) ov[pos] = key2f(comp_key(v));
                     }
                 }
-                for (int j = take + c.tid; j < k; j += RF_NT) {  // len < k: -1 padding
-                    o[j] = -1;
-                    if (ov) ov[j] = 0.f;
-                }
+                if (!tie_fill)
+                    for (int j = take + c.tid; j < k; j += RF_NT) {  // len < k: -1 padding
+                        o[j] = -1;
+                        if (ov) ov[j] = 0.f;
+                    }
             }
+        }
+        if (ok && tie_fill) {
+            // positions [take, K): the first K - take elements of the row equal to the tied
+            // key, in index order — thread t scans 8 consecutive elements per step, an
+            // exclusive scan orders the matches; fewer than needed: the tie is not the K-th
+            // key after all and the row goes to the fixup list
+            int32_t* o = out + (int64_t)r * k;
+            float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
+            const int need = K - take;
+            int found = 0;
+            for (int base = 0; base < p.n && found < need; base += 8 * RF_NT) {
+                const int i0 = base + 8 * c.tid;
+                uint32_t hit = 0u;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (i0 + j < p.n && f2key(__ldg(p.x + i0 + j)) == tie) hit |= 1u << j;
+                uint32_t tot;
+                uint32_t pos = (uint32_t)(take + found) + group_excl_scan(c, (uint32_t)__popc(hit), tot);
+                for (; hit; hit &= hit - 1u, ++pos)
+                    if (pos < (uint32_t)K) {
+                        o[pos] = i0 + __ffs(hit) - 1;
+                        if (ov) ov[pos] = key2f(tie);
+                    }
+                found += (int)tot;
+            }
+            ok = found >= need;
+            levels = 0;
+            ftc = total;
         }
         if (trivial && p.n == 0) {
             int32_t* o = out + (int64_t)r * k;
@@ -335,8 +374,8 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 s.secant_iters = g.iters;  // Phase-2 probes (gvr_guess_kernel)
                 s.snap_iters = 0;
                 s.cand_count = trivial ? p.n : ftc;
-                s.done_kind = trivial ? GVR_DONE_TRIVIAL : GVR_DONE_CONVERGED;
-                s.global_passes = 1;
+                s.done_kind = trivial ? GVR_DONE_TRIVIAL : tie_fill ? GVR_DONE_TIEFILL : GVR_DONE_CONVERGED;
+                s.global_passes = tie_fill ? 2 : 1;  // the tie scan reads (part of) the row again
                 s.raises = levels > 1 ? levels - 1 : 0;  // Phase-4 histogram narrowings (R32)
                 s.buffer_count = trivial ? 0 : ftc;
                 s.cluster = 1;

@@ -53,7 +53,7 @@ def _heads(R, stride):
     return [((16 - ((r * stride * 4) & 15)) & 15) >> 2 for r in range(R)]
 
 
-def _assert_replay(host, lens, prev, st, k=K, stride_guess=8, rows=None):
+def _assert_replay(host, lens, prev, st, k=K, stride_guess=8, rows=None, filter_path=False):
     """Kernel Phase-2 statistics == the CPU replay, row by row."""
     R, S = host.shape
     heads = _heads(R, S)
@@ -62,7 +62,8 @@ def _assert_replay(host, lens, prev, st, k=K, stride_guess=8, rows=None):
         n = int(lens[r])
         if n <= k:
             continue
-        rep = P2.replay_row(host[r, :n], None if prev is None else prev[r], k, head=heads[r], stride=stride_guess)
+        rep = P2.replay_row(host[r, :n], None if prev is None else prev[r], k, head=heads[r], stride=stride_guess,
+                            filter_path=filter_path)
         got = (int(_col(st, "tc_key")[r]) & 0xFFFFFFFF, int(_col(st, "secant_iters")[r]),
                int(_col(st, "phase2_exit")[r]), int(_col(st, "sample_count")[r]))
         exp = (rep["Tc"], rep["I"], rep["done"], rep["count"] if rep["done"] else 0)
@@ -124,7 +125,7 @@ def test_phase2_stats_match_replay_batch_paths(gvr, path):
     got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev),
                    opts=gvr.GvrOptions(float("nan"), 0, 0, 0, path))
     _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
-    _assert_replay(host, lens, prev, st)
+    _assert_replay(host, lens, prev, st, filter_path=path == 0)
 
 
 # ------------------------------------------------------------------ high alpha
@@ -146,7 +147,7 @@ def test_high_alpha_filter_path_one_pass_no_fixup(gvr, rho):
     ref = oracle.topk_batched(host[:20], K, row_lens=lens[:20])
     alpha = np.mean([len(np.intersect1d(prev[r], ref[r])) / K for r in range(20)])
     assert alpha > 0.5
-    _assert_replay(host, lens, prev, st, rows=range(0, 300, 37))
+    _assert_replay(host, lens, prev, st, rows=range(0, 300, 37), filter_path=True)
 
 
 # ------------------------------------------------------------------ sizes on the filter path

@@ -177,15 +177,31 @@ def test_phase2_ties_exit_takes_lo_anchor():
     assert (T, it, done, c) == (P2.key(v0), 1, P2.DONE_TIES, 4096)
 
 
-def test_phase2_exhausted_exit_takes_lo_anchor():
+def test_phase2_exhausted_exit_takes_sample_rank():
     """Two values far apart in key space: every probe lands on one side; after MAX_ITERS
-    probes the search stops with the lo anchor (hits above the window: the safe side)."""
+    probes the exact finisher over the sample (R12) takes the key of rank ceil(f_t) —
+    here the lower value (only 96 samples hold the upper one), whose hits are all 4096."""
     n = 100_000
     sk = P2.keys(np.r_[np.zeros(4000, np.float32), np.ones(96, np.float32)])
     T, it, done, c = P2.phase2(sk, (P2.key(0.0), P2.key(1.0), np.float32(0.5), K), n, K)
     L, H, _ = P2.window(n, K)
-    assert done == P2.DONE_EXHAUSTED and it == P2.MAX_ITERS and c > H
-    assert c == int(np.count_nonzero(sk >= np.uint32(T)))
+    assert done == P2.DONE_EXHAUSTED and it == P2.MAX_ITERS
+    assert T == P2.key(0.0) and c == 4096
+
+
+def test_phase2_exhausted_rank_select_on_a_skewed_sample():
+    """The finisher's key has exactly rank ceil(f_t) among distinct sample keys."""
+    n = 100_000
+    L, H, ft = P2.window(n, K)
+    rank = (L + H + 1) // 2
+    vals = np.exp(np.linspace(0, 30, 4096)).astype(np.float32)  # distinct, very skewed
+    sk = P2.keys(vals)
+    # force exhaustion: anchors far from the window with a probe budget of 0 secants
+    T, it, done, c = P2.phase2(sk, None, n, K)
+    if done == P2.DONE_EXHAUSTED:
+        assert c == rank and T == int(np.sort(sk)[::-1][rank - 1])
+    else:
+        assert done == P2.DONE_WINDOW and L <= c <= H
 
 
 def test_phase2_no_guess_uses_sample_statistics():
