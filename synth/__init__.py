@@ -195,7 +195,11 @@ def appendix_e_row(n: int, seed: int, am: float = 0.1, d_rope: int = 64, device=
 # ----------------------------------------------------------------------------- test distributions
 DISTRIBUTIONS = ("uniform", "normal", "lognormal", "heavy_tail", "ties90", "all_equal",
                  "few_distinct", "signed_zero_mix", "with_inf", "sorted_asc", "sorted_desc",
-                 "negative", "tiny_range")
+                 "negative", "tiny_range", "beta", "weibull", "logistic")
+# the score shapes fitted to the real DSV3.2 layers (Table 7):
+# beta (bounded, peaked: L21/L40/L41), weibull (right-skewed: L22/L60), logistic
+# (heavy-tailed: L1), lognormal (heterogeneous: L0)
+TABLE7_SHAPES = ("beta", "weibull", "logistic", "lognormal")
 
 
 def dist_row(kind: str, n: int, seed: int) -> np.ndarray:
@@ -232,6 +236,12 @@ def dist_row(kind: str, n: int, seed: int) -> np.ndarray:
         x = -rng.lognormal(1.0, 0.5, n)
     elif kind == "tiny_range":
         x = 1.0 + rng.integers(0, 3000, n) * np.finfo(np.float32).eps
+    elif kind == "beta":
+        x = rng.beta(2.0, 5.0, n)
+    elif kind == "weibull":
+        x = rng.weibull(1.5, n)
+    elif kind == "logistic":
+        x = rng.logistic(0.0, 1.0, n)
     else:
         raise ValueError(kind)
     return np.ascontiguousarray(x.astype(np.float32))
