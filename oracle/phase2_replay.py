@@ -217,15 +217,14 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
 def replay_row(x: np.ndarray, guess, k: int, head: int = 0, stride: int = 8, z=Z, max_secant: int = MAX_SECANT,
                filter_path: bool = False):
     """Phases 1-2 of one row as the guess kernel runs them (head: the row's scalars before
-    its first 16-byte boundary; stride: the guess stride, used for n >= 32 k).  Returns a
+    its first 16-byte boundary; stride: the guess stride, every row).  Returns a
     dict with the collect threshold key Tc, I, done (Phase-2 exit), window (L, H), the
     sample count at Tc and the Phase-1 tuple p1 = (pmin key, pmax key, pmean, count)."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     n = x.size
     if n <= CAP_ALL:
         return dict(Tc=0, I=0, done=DONE_ALL, L=0, H=0, count=0)
-    st = stride if n >= 32 * k else 1
-    p1 = phase1(x, guess, k, st)
+    p1 = phase1(x, guess, k, stride)
     sv = x[sample_positions(n, head)]
     sk = keys(sv)
     if p1 is None:

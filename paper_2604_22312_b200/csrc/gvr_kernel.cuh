@@ -621,8 +621,8 @@ constexpr float P2_Z_DEFAULT = 4.5f;
 // R19, R29, R34-R36).  Every fp32 operation is explicit round-to-nearest in a fixed
 // order, so the CPU replay reproduces T_c, I and the exit kind bit for bit.
 //   Phase 1: the guessed values x[q], q = prev[m] for the guessed ranks m of slots
-//     i = t + 256 j (thread t): m_i = 8 gs floor(i / 8) + i % 8 < k (R29) -> pmin / pmax
-//     (keys), pmean = sum / count (Eq. 4).
+//     i = t + 256 j (thread t): m_i = 8 gs floor(i / 8) + i % 8 < k (R29; load_guess_idx)
+//     -> pmin / pmax (keys), pmean = sum / count (Eq. 4).
 //     No valid guess -> the statistics of the row sample.
 //   Sample: chunk t (16 contiguous floats of the 16-byte aligned body, chunk start
 //     16 * floor(t * nch / 256) of nch = body / 16 chunks) in registers, as keys.
@@ -665,12 +665,31 @@ __device__ __forceinline__ uint32_t sample_rank_key16(G& c, const uint32_t (&sk)
     return prefix;
 }
 
+// The guess indices Phase 1 reads (they do not depend on the row length, so callers issue
+// these loads first): slot i = tid + 256 j holds guessed rank m_i = 8 gs (i / 8) + i % 8
+// when m_i < k — blocks of 8 consecutive ranks every 8 gs ranks, one 32-byte sector of
+// indices per block (gs = guess_stride; 1 = every rank; R29); -1 for unused slots.
+constexpr int GUESS_PER_THREAD = KMAX / 256;
 template <class G>
-__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t* pr, int k, const GvrParams& prm,
-                                            int32_t* sh256)
+__device__ __forceinline__ void load_guess_idx(const G& c, const int32_t* pr, int k, const GvrParams& prm,
+                                               int32_t (&gi)[GUESS_PER_THREAD])
+{
+    static_assert(G::N == 256, "eight guess slots per thread");
+    const int gs = prm.guess_stride;
+#pragma unroll
+    for (int j = 0; j < GUESS_PER_THREAD; ++j) {
+        const int i = c.tid + j * G::N;
+        const int m = 8 * gs * (i >> 3) + (i & 7);
+        gi[j] = (pr && m < k) ? __ldg(pr + m) : -1;
+    }
+}
+
+template <class G>
+__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t (&gi)[GUESS_PER_THREAD], int k,
+                                            const GvrParams& prm, int32_t* sh256)
 {
     static_assert(G::N == 256, "one sample chunk per thread");
-    constexpr int GPT = KMAX / G::N;  // 8 guessed positions per thread
+    constexpr int GPT = GUESS_PER_THREAD;  // 8 guessed positions per thread
     GuessOut g;
     if (p.n <= GVR_CAP) {  // the whole row fits in B: collect everything, no search
         g.Tc = 0u;
@@ -697,31 +716,15 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
         sv[4 * q + 2] = v.z;
         sv[4 * q + 3] = v.w;
     }
-    // slot i = tid + 256 j holds guessed rank m_i = 8 gs (i / 8) + i % 8 when m_i < k:
-    // blocks of 8 consecutive ranks every 8 gs ranks (one 32-byte sector of indices per
-    // block), gs = guess_stride for rows with n >= 32 k, else 1 (every rank; R29)
-    const int gs = p.n >= 32 * k ? prm.guess_stride : 1;
     float gv[GPT];
     uint32_t valid = 0;
-    if (pr) {
-        int32_t gi[GPT];
 #pragma unroll
-        for (int j = 0; j < GPT; ++j) {
-            const int i = c.tid + j * G::N;
-            const int m = 8 * gs * (i >> 3) + (i & 7);
-            gi[j] = m < k ? __ldg(pr + m) : -1;
+    for (int j = 0; j < GPT; ++j) {
+        gv[j] = 0.f;
+        if (gi[j] >= 0 && gi[j] < p.n) {
+            gv[j] = ld_gather(p.x + gi[j]);
+            valid |= 1u << j;
         }
-#pragma unroll
-        for (int j = 0; j < GPT; ++j) {
-            gv[j] = 0.f;
-            if (gi[j] >= 0 && gi[j] < p.n) {
-                gv[j] = ld_gather(p.x + gi[j]);
-                valid |= 1u << j;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < GPT; ++j) gv[j] = 0.f;
     }
     uint32_t sk[P2_CHUNK];
     uint32_t smin = 0xffffffffu, smax = 0u;
@@ -746,7 +749,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     }
     group_red4<R_MIN, R_MAX, R_ADD, R_MAX>(c, kmn, kmx, cnt, smax);
     smin = group_red1<R_MIN>(c, smin);
-    bool complete = cnt == (uint32_t)k && gs == 1;
+    bool complete = cnt == (uint32_t)k && prm.guess_stride == 1;
     if (cnt == 0) {  // no valid guess: statistics of the row sample (R7)
         sum = 0.f;
 #pragma unroll
@@ -865,6 +868,8 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     GuessGroup c;
     c.init(threadIdx.x, scratch);
     const int r = blockIdx.x;
+    int32_t gi[GUESS_PER_THREAD];  // issued first: the guess indices do not depend on the row length
+    load_guess_idx(c, prev ? prev + (int64_t)r * k : nullptr, k, prm, gi);
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
     // batch filter path: a row with no tiles never reaches the filter kernel; it goes to
     // the ready queue now (the refine kernel emits it from the row itself)
@@ -874,7 +879,7 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
         return;
     }
     __shared__ int32_t sh[256];
-    GuessOut g = phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm, sh);
+    GuessOut g = phase12(c, p, gi, k, prm, sh);
     // filter path, a ties exit: collect the keys strictly above the tie; when they are
     // fewer than K the refine kernel fills the rest with the tie's lowest indices (R37)
     if (bq.queue && g.exit == GVR_P2_TIES && g.tie < 0xffffffffu) g.Tc = g.tie + 1u;
@@ -948,8 +953,13 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
         st[2] = p.n;
     } else {
         // ---------------- Phases 1-2: in gvr_guess_kernel (batch paths) or here (fused)
-        gq = gp ? gp[r] : phase12(c, p, prev ? prev + (int64_t)r * k : nullptr, k, prm,
-                                  reinterpret_cast<int32_t*>(smem + G_OFF_RHIST));
+        if (gp) {
+            gq = gp[r];
+        } else {
+            int32_t gi[GUESS_PER_THREAD];
+            load_guess_idx(c, prev ? prev + (int64_t)r * k : nullptr, k, prm, gi);
+            gq = phase12(c, p, gi, k, prm, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST));
+        }
         RowMeta m;
         m.Tc = short_known ? gq.tmin : gq.Tc;
         if (short_known) passes = 2;
@@ -1243,7 +1253,9 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
         st[2] = pw.n;
     } else {
         // ---------------- Phase 1 (every CTA, identical result) and the slice stream
-        gq = phase12(c, pw, prev ? prev + (int64_t)r * k : nullptr, k, prm, rhist);
+        int32_t gi[GUESS_PER_THREAD];
+        load_guess_idx(c, prev ? prev + (int64_t)r * k : nullptr, k, prm, gi);
+        gq = phase12(c, pw, gi, k, prm, rhist);
         if (phase_ts) tsr[TS_PHASE1] = clock64();
         uint32_t Tc = gq.Tc, kmax = 0u, extras = 0u, Tm = 0u, kmx = 0u, T = 0u, tot = 0, pre = 0;
         int fill = 0, raises_all = 0;

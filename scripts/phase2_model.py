@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--layers", default="0-60")
     ap.add_argument("--rhos", default=None)
     ap.add_argument("--draft", type=int, default=1)
-    ap.add_argument("--stride", type=int, default=8)
+    ap.add_argument("--stride", type=int, default=8)  # guess stride (every row)
     a = ap.parse_args()
     lo, hi = (int(v) for v in a.layers.split("-"))
     rhos = [float(v) for v in a.rhos.split(",")] if a.rhos else None
