@@ -247,3 +247,33 @@ def test_radix2_baseline_ties_and_decode_rows(gvr):
     idx = gvr.radix2_topk(torch.from_numpy(host).cuda(), K, row_lens=b["row_lens"])
     torch.cuda.synchronize()
     _assert_exact(idx.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens))
+
+
+# ------------------------------------------------------------------ ultra-long rows
+@pytest.mark.parametrize("n", [1 << 20, 1 << 22])
+def test_ultra_long_single_rows(gvr, n):
+    """Rows far beyond any CTA's or cluster's shared memory (1M and 4M elements): the
+    cluster kernel streams its slices (the row is never resident); exact."""
+    import torch
+    rows = [synth.dist_row(kind, n, seed=2900 + i) for i, kind in enumerate(("normal", "lognormal"))]
+    host = np.stack(rows)
+    lens = np.full(2, n, np.int32)
+    dev = torch.device("cuda:0")
+    prev = np.stack([synth.guess("random", r, K, 2901) for r in rows]).astype(np.int32)
+    got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev))
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+
+
+def test_ultra_long_batch_filter_path(gvr):
+    """300 rows of 512K elements (more than one wave: the filter path, each row split over
+    several filter CTAs)."""
+    import torch
+    R, n = 300, 1 << 19
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(3000)
+    s = torch.randn((R, n), generator=g, device=dev)
+    prev = torch.randint(0, n, (R, K), generator=g, device=dev, dtype=torch.int32)
+    lens = torch.full((R,), n, dtype=torch.int32, device=dev)
+    got, st = _run(gvr, s, lens, prev)
+    _assert_exact(got, oracle.topk_batched(s.cpu().numpy(), K), st)
+    assert (_col(st, "global_passes") == 1).all()
