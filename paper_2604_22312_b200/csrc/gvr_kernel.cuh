@@ -301,10 +301,14 @@ __device__ __forceinline__ void write_candidates(const Buf& B, const float* sp, 
 // The streaming pass of one row (row body through the ring; the <= 6 unaligned head /
 // tail scalars exactly).  Collects B ⊇ {key >= Tc}, superset only by NaN / -0-against-+0
 // entries counted in `extras`.  Returns 0, or 1 on massive ties (the remaining tiles are
-// still waited for, so no copy is in flight when the ring is reused).
+// still waited for, so no copy is in flight when the ring is reused).  pbits: the phase
+// parity of each stage's mbarrier before this pass (bit s for stage s); the ring's
+// barriers are initialised once per CTA and their phases carried across passes and rows
+// (no mbarrier re-initialisation while copies of earlier passes are tracked), updated here
+// by the number of tiles each stage received.
 __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const RowPlan& p, const Buf& B,
                                           int32_t* rhist, uint32_t& Tc, int& fill, int K, int& raises, uint32_t& kmax,
-                                          uint32_t& extras, uint32_t& tie_key)
+                                          uint32_t& extras, uint32_t& tie_key, uint32_t& pbits)
 {
     int* fillp = c.misc + 16;     // reservation cursor
     int* failbase = c.misc + 17;  // lowest failed reservation of the round
@@ -339,10 +343,10 @@ __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const R
     for (int rd = 0; rd < nrounds; ++rd) {
         const int t0 = rd * ROUND_STAGES;
         const int s0 = t0 % NSTAGE;
-        const uint32_t par = (uint32_t)(t0 / NSTAGE) & 1u;
+        const uint32_t lap = (uint32_t)(t0 / NSTAGE);
         const int nf = min(ROUND_FLOATS, p.nfl - t0 * STAGE_FLOATS);  // floats in this round
-        mbar_wait(ring.full(s0), par);
-        if (t0 + 1 < p.ntiles) mbar_wait(ring.full(s0 + 1), par);
+        mbar_wait(ring.full(s0), (lap ^ (pbits >> s0)) & 1u);
+        if (t0 + 1 < p.ntiles) mbar_wait(ring.full(s0 + 1), (lap ^ (pbits >> (s0 + 1))) & 1u);
         const float* sp = ring.stage(s0);
         const int ibase = p.idx0 + p.head + t0 * STAGE_FLOATS + lb;
         bool failed_here = false;
@@ -419,6 +423,9 @@ __device__ __forceinline__ int stream_row(GvrGroup& c, const Ring& ring, const R
                 if (t0 + q + NSTAGE < p.ntiles) ring.issue(p, t0 + q + NSTAGE);
     }
     fill = *fillp;
+#pragma unroll
+    for (int st = 0; st < NSTAGE; ++st)  // tiles t = st, st + NSTAGE, ... each completed one phase
+        if (p.ntiles > st) pbits ^= ((uint32_t)((p.ntiles - 1 - st) / NSTAGE + 1) & 1u) << st;
     c.sync();  // every thread has read the cursor before the scratch is reused
     return rc;
 }
@@ -544,10 +551,12 @@ __device__ __forceinline__ void refine_row(GvrGroup& c, const Buf& B, const Work
                 c.sync();
                 break;
             }
-            // exact narrowing inside bin b
+            // exact narrowing inside bin b (every thread has read hist[b] before the next
+            // level clears the histogram)
             base = lo_b;
             width = bw;
             s = s > 11 ? s - 11 : 0;
+            c.sync();
         }
     } else {
         uint32_t kmin = 0xffffffffu;
@@ -916,7 +925,7 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
                                       const int32_t* __restrict__ row_lens, int k, int32_t* out, float* out_val,
                                       gvr_row_stats* stats, const GvrParams& prm, const GuessOut* __restrict__ gp,
                                       const int32_t* prev, long long* phase_ts, int r, bool reinit,
-                                      bool short_known = false)
+                                      uint32_t& pbits, bool short_known = false)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const Ring ring{reinterpret_cast<float*>(smem + G_OFF_RING), reinterpret_cast<uint64_t*>(smem + G_OFF_BARS),
@@ -930,13 +939,15 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
     const int K = k;
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
     const long long ts0 = phase_ts ? clock64() : 0ll;
-    if (reinit) c.sync();  // every wait on the previous row's barriers is over
+    if (reinit) {
+        fence_proxy_async_smem();  // the previous row's work area (aliasing the ring) before the TMA refill
+        c.sync();                  // every wait on the previous row's barriers is over
+    }
     if (c.tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) {
-            if (reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(ring.full(s)) : "memory");
-            mbar_init(ring.full(s), 1);
+        if (!reinit) {  // the CTA's first row: the barriers start at phase 0
+            for (int s = 0; s < NSTAGE; ++s) mbar_init(ring.full(s), 1);
+            fence_mbar_init();
         }
-        fence_mbar_init();
         for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);  // the first 64 KB load during Phase 1
     }
     const RowGeom g = make_geom(p.x, p.n);
@@ -967,7 +978,7 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
         // ---------------- streaming pass (HBM read once, TMA ring)
         uint32_t kmax = 0u, extras = 0u, tie_key = 0u;
         const int rc = stream_row(c, ring, p, B, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST), m.Tc, m.fill, K, raises,
-                                  kmax, extras, tie_key);
+                                  kmax, extras, tie_key, pbits);
         group_red2<R_MAX, R_ADD>(c, kmax, extras);
         m.kmax = kmax;
         m.extras = extras;
@@ -990,21 +1001,16 @@ __device__ __forceinline__ void topk_row(const float* __restrict__ scores, int64
             // f(T_c) < K (the threshold overshot the K-th value): stream the row once more at
             // a threshold that cannot undershoot — pmin of a complete guess, else -inf —
             // with the usual raises keeping >= K (R30); bounded at two HBM passes
+            fence_proxy_async_smem();
             c.sync();
-            if (c.tid == 0) {
-                for (int s2 = 0; s2 < NSTAGE; ++s2) {
-                    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(ring.full(s2)) : "memory");
-                    mbar_init(ring.full(s2), 1);
-                }
-                fence_mbar_init();
+            if (c.tid == 0)
                 for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);
-            }
             m.Tc = gq.tmin;
             kmax = 0u;
             extras = 0u;
             uint32_t tie2 = 0u;
             const int rc2 = stream_row(c, ring, p, B, reinterpret_cast<int32_t*>(smem + G_OFF_RHIST), m.Tc, m.fill, K,
-                                       raises, kmax, extras, tie2);
+                                       raises, kmax, extras, tie2, pbits);
             group_red2<R_MAX, R_ADD>(c, kmax, extras);
             m.kmax = kmax;
             m.extras = extras;
@@ -1083,8 +1089,9 @@ gvr_topk_kernel(const float* __restrict__ scores, int64_t stride, const int32_t*
     // Fused mode (gp == nullptr, batches of at most one wave): CTA b processes row b and
     // runs Phase 1 itself while its first tiles load.
     if (gp) asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint32_t pbits = 0u;
     topk_row(scores, stride, row_lens, k, out, out_val, stats, prm, gp, prev, phase_ts,
-             gp ? order[blockIdx.x] : (int)blockIdx.x, false);
+             gp ? order[blockIdx.x] : (int)blockIdx.x, false, pbits);
     fixup_done(ctl, BatchQueue{}, threadIdx.x);
 }
 
@@ -1100,11 +1107,12 @@ gvr_fixup_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
 {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the refine grid's fixup list is complete
     const int nfix = ld_relaxed(bq.qctl + Q_NFIX);
+    uint32_t pbits = 0u;  // stage phase parities carried across this CTA's rows
     for (int li = (int)blockIdx.x; li < nfix; li += (int)gridDim.x)
     {
         const uint32_t e = (uint32_t)__ldcg(bq.fixlist + li);  // row | (f(T_c) < K known) << 31
         topk_row(scores, stride, row_lens, k, out, out_val, stats, prm, gp, prev, phase_ts, (int)(e & 0x7fffffffu),
-                 li != (int)blockIdx.x, (e >> 31) != 0u);
+                 li != (int)blockIdx.x, pbits, (e >> 31) != 0u);
     }
     fixup_done(ctl, bq, threadIdx.x);
 }
@@ -1262,19 +1270,15 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
         bool ok = false;
         ChunkCounts cc;
         int32_t* lcx = cl.map_shared_rank(cx, 0);
+        uint32_t pbits = 0u;  // stage phase parities (stream_row)
         for (int pass = 0;; ++pass) {
             if (pass == 1) {
                 // f(T_m) < K: every slice is streamed once more at a threshold that cannot
                 // undershoot (R30)
+                fence_proxy_async_smem();  // the exchange area (inside the ring) before the TMA refill
                 c.sync();
-                if (c.tid == 0) {
-                    for (int s2 = 0; s2 < NSTAGE; ++s2) {
-                        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(ring.full(s2)) : "memory");
-                        mbar_init(ring.full(s2), 1);
-                    }
-                    fence_mbar_init();
+                if (c.tid == 0)
                     for (int t = 0; t < NSTAGE && t < p.ntiles; ++t) ring.issue(p, t);
-                }
                 Tc = gq.tmin;
                 kmax = 0u;
                 extras = 0u;
@@ -1282,7 +1286,7 @@ gvr_topk_cluster_kernel(const float* __restrict__ scores, int64_t stride, const 
                 ++passes;
             }
             uint32_t tie_unused = 0u;  // cluster slices: ties end in the leader's fallback
-            const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras, tie_unused);
+            const int rc = stream_row(c, ring, p, B, rhist, Tc, fill, K, raises, kmax, extras, tie_unused, pbits);
             group_red2<R_MAX, R_ADD>(c, kmax, extras);
             // ---------------- merge across the cluster (DSMEM)
             cl.sync();  // every slice streamed; rings idle

@@ -277,3 +277,19 @@ def test_ultra_long_batch_filter_path(gvr):
     got, st = _run(gvr, s, lens, prev)
     _assert_exact(got, oracle.topk_batched(s.cpu().numpy(), K), st)
     assert (_col(st, "global_passes") == 1).all()
+
+
+def test_fixup_kernel_short_lists(gvr):
+    """A Phase-2 window aimed below the K-th value (window_z = -8) leaves every filter-path
+    list short: the refine hands all 300 rows to the fixup kernel, which streams each once
+    more at the second-pass threshold (R30, skipping the known-short first stream)."""
+    import torch
+    R, n = 300, 9_000
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(3100)
+    s = torch.randn((R, n), generator=g, device=dev)
+    prev = torch.randint(0, n, (R, K), generator=g, device=dev, dtype=torch.int32)
+    lens = torch.full((R,), n, dtype=torch.int32, device=dev)
+    got, st = _run(gvr, s, lens, prev, opts=gvr.GvrOptions(-8.0, 0, 0, 0, 0))
+    _assert_exact(got, oracle.topk_batched(s.cpu().numpy(), K), st)
+    assert (_col(st, "global_passes") == 2).all(), st[:3].tolist()
