@@ -182,6 +182,36 @@ gvr_status radix2_topk_batched_ex(const float* scores, int64_t row_stride, const
                                   int32_t num_rows, int32_t k, int32_t* out_idx, cudaStream_t stream,
                                   float* out_val, gvr_row_stats* stats);
 
+/* ---- DSA indexer (Eq. 1, lines 78-81) -------------------------
+ * I_t[i] = sum_{j<64} w[r][j] * ReLU(q[r][j] . keys[set][i]) for i < row_lens[r], with
+ * bf16 inputs and fp32 accumulation on tensor cores.  keys: device bf16
+ * [num_sets][n_max][128] (RoPE applied, the indexer key cache); row_set: device int32
+ * [num_rows], the key set of row r (the draft rows of an MTP request share one); row_lens:
+ * device int32 [num_rows] or NULL (= n_max), each <= n_max; q: device bf16
+ * [num_rows][64][128]; w: device fp32 [num_rows][64].  The score arithmetic is one fixed
+ * order shared by every indexer entry point, so the scores are bit-identical across them.
+ *
+ * gvr_indexer_scores: the scores themselves, out: device fp32 [num_rows][out_stride]
+ * (out_stride >= n_max; entries past row_lens[r] untouched). */
+gvr_status gvr_indexer_scores(const void* keys, int64_t n_max, const int32_t* row_set, const int32_t* row_lens,
+                              const void* q, const float* w, int32_t num_rows, float* out, int64_t out_stride,
+                              cudaStream_t stream);
+
+/* gvr_indexer_topk_batched: the fused indexer -> GVR Top-K: the exact
+ * ordered Top-K of the rows' indexer scores (the gvr_indexer_scores values) without
+ * writing the score rows: Phases 1-2 score only the guessed and the 4096 sample positions,
+ * the one pass over the key cache scores each 256-key step in shared memory and keeps the
+ * candidates >= T_c, and the refine kernel selects from the candidate lists.
+ * score_scratch: device fp32 [num_rows][n_max], 16-byte aligned, caller-owned — written
+ * only for the rows the lists cannot finish (rows of <= k keys, massive ties, a threshold
+ * overshoot), which are then finished from their materialised scores.  n_max must be a
+ * multiple of 4.  prev_topk, k, out_idx as in gvr_topk_batched.  Same errors as
+ * gvr_topk_batched, plus GVR_ERR_UNSUPPORTED for n_max % 4 != 0 or a misaligned scratch. */
+gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32_t* row_set,
+                                    const int32_t* row_lens, const void* q, const float* w,
+                                    int32_t num_rows, const int32_t* prev_topk, int32_t k,
+                                    int32_t* out_idx, float* score_scratch, cudaStream_t stream);
+
 /* ---- host-buffer entry point (end-to-end use) ------------------------------------
  * A workspace owns device buffers for up to max_rows rows of row_stride elements and
  * k outputs.  gvr_topk_batched_host copies HOST scores/row_lens/prev (pinned memory

@@ -58,6 +58,8 @@ def _load():
         "radix_topk_batched": [vp, i64, vp, i32, i32, vp, vp],
         "radix_topk_batched_ex": [vp, i64, vp, i32, i32, vp, vp, vp, vp],
         "radix2_topk_batched": [vp, i64, vp, i32, i32, vp, vp],
+        "gvr_indexer_scores": [vp, i64, vp, vp, vp, vp, i32, vp, i64, vp],
+        "gvr_indexer_topk_batched": [vp, i64, vp, vp, vp, vp, i32, vp, i32, vp, vp, vp],
         "radix2_topk_batched_ex": [vp, i64, vp, i32, i32, vp, vp, vp, vp],
         "gvr_workspace_create": [i32, i64, i32, ctypes.POINTER(vp)],
         "gvr_workspace_destroy": [vp],
@@ -236,6 +238,51 @@ def radix2_topk_ex(scores, k: int = MAX_K, row_lens=None, out=None, values=True,
     _check(_load().radix2_topk_batched_ex(_ptr(scores), stride, _ptr(row_lens), R, k, _ptr(out),
                                           _stream_ptr(stream), _ptr(val), _ptr(st)))
     return out, val, st
+
+
+def _indexer_args(keys, row_set, q, w, row_lens):
+    torch = _torch()
+    if keys.dtype != torch.bfloat16 or keys.dim() != 3 or keys.shape[2] != 128 or not keys.is_contiguous() \
+            or not keys.is_cuda:
+        raise GvrError("keys must be a contiguous bf16 CUDA tensor [sets, n_max, 128]")
+    R = row_set.shape[0]
+    if row_set.dtype != torch.int32 or row_set.dim() != 1 or not row_set.is_cuda:
+        raise GvrError("row_set must be int32 CUDA [R]")
+    if q.dtype != torch.bfloat16 or tuple(q.shape) != (R, 64, 128) or not q.is_contiguous() or not q.is_cuda:
+        raise GvrError("q must be a contiguous bf16 CUDA tensor [R, 64, 128]")
+    if w.dtype != torch.float32 or tuple(w.shape) != (R, 64) or not w.is_contiguous() or not w.is_cuda:
+        raise GvrError("w must be a contiguous fp32 CUDA tensor [R, 64]")
+    if row_lens is not None and (row_lens.dtype != torch.int32 or tuple(row_lens.shape) != (R,) or not row_lens.is_cuda):
+        raise GvrError("row_lens must be int32 CUDA [R]")
+    return R, keys.shape[1]
+
+
+def indexer_scores(keys, row_set, q, w, row_lens=None, out=None, stream=None):
+    """DSA indexer scores (Eq. 1) on tensor cores: fp32 [R, n_max]."""
+    torch = _torch()
+    R, n_max = _indexer_args(keys, row_set, q, w, row_lens)
+    if out is None:
+        out = torch.zeros((R, n_max), dtype=torch.float32, device=keys.device)
+    _check(_load().gvr_indexer_scores(_ptr(keys), n_max, _ptr(row_set), _ptr(row_lens), _ptr(q), _ptr(w), R,
+                                      _ptr(out), out.stride(0), _stream_ptr(stream)))
+    return out
+
+
+def indexer_topk(keys, row_set, q, w, k: int = MAX_K, row_lens=None, prev=None, out=None, scratch=None,
+                 stream=None):
+    """Fused indexer -> GVR Top-K: the exact ordered Top-K of the indexer scores without
+    writing them (scratch fp32 [R, n_max] is touched only for rows the lists cannot finish)."""
+    torch = _torch()
+    R, n_max = _indexer_args(keys, row_set, q, w, row_lens)
+    if prev is not None and (prev.dtype != torch.int32 or tuple(prev.shape) != (R, k) or not prev.is_contiguous()):
+        raise GvrError("prev must be a contiguous int32 CUDA tensor [R, k]")
+    if out is None:
+        out = torch.empty((R, k), dtype=torch.int32, device=keys.device)
+    if scratch is None:
+        scratch = torch.empty((R, n_max), dtype=torch.float32, device=keys.device)
+    _check(_load().gvr_indexer_topk_batched(_ptr(keys), n_max, _ptr(row_set), _ptr(row_lens), _ptr(q), _ptr(w), R,
+                                            _ptr(prev), k, _ptr(out), _ptr(scratch), _stream_ptr(stream)))
+    return out
 
 
 class Workspace:

@@ -693,48 +693,16 @@ __device__ __forceinline__ void load_guess_idx(const G& c, const int32_t* pr, in
     }
 }
 
+// Phases 1-2 from the values: gv[j] the guessed value of slot j (valid bit j), sv the
+// thread's 16 sample values; n the row length.  Shared by phase12 (values read from the
+// score row) and the fused indexer path (values computed from the keys, indexer_kernel.cuh).
 template <class G>
-__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t (&gi)[GUESS_PER_THREAD], int k,
-                                            const GvrParams& prm, int32_t* sh256)
+__device__ __forceinline__ GuessOut phase12_core(G& c, int n, const float (&gv)[GUESS_PER_THREAD], uint32_t valid,
+                                                 const float (&sv)[P2_CHUNK], int k, const GvrParams& prm,
+                                                 int32_t* sh256)
 {
-    static_assert(G::N == 256, "one sample chunk per thread");
-    constexpr int GPT = GUESS_PER_THREAD;  // 8 guessed positions per thread
+    constexpr int GPT = GUESS_PER_THREAD;
     GuessOut g;
-    if (p.n <= GVR_CAP) {  // the whole row fits in B: collect everything, no search
-        g.Tc = 0u;
-        g.tie = 0u;
-        g.T0 = 0u;
-        g.tmin = 0u;
-        g.top = 0xffffffffu;
-        g.t0_ok = 0;
-        g.iters = 0;
-        g.exit = GVR_P2_ALL;
-        g.scount = 0;
-        return g;
-    }
-    // ---- loads: the sample chunk, the guess indices, then the guessed values
-    const int nch = p.nfl / P2_CHUNK;  // >= 376 for n > GVR_CAP
-    const float4* sp4 =
-        reinterpret_cast<const float4*>(p.x + p.head + P2_CHUNK * (int)(((int64_t)c.tid * nch) >> 8));
-    float sv[P2_CHUNK];
-#pragma unroll
-    for (int q = 0; q < P2_CHUNK / 4; ++q) {
-        const float4 v = ldg_sample(sp4 + q);
-        sv[4 * q] = v.x;
-        sv[4 * q + 1] = v.y;
-        sv[4 * q + 2] = v.z;
-        sv[4 * q + 3] = v.w;
-    }
-    float gv[GPT];
-    uint32_t valid = 0;
-#pragma unroll
-    for (int j = 0; j < GPT; ++j) {
-        gv[j] = 0.f;
-        if (gi[j] >= 0 && gi[j] < p.n) {
-            gv[j] = ld_gather(p.x + gi[j]);
-            valid |= 1u << j;
-        }
-    }
     uint32_t sk[P2_CHUNK];
     uint32_t smin = 0xffffffffu, smax = 0u;
 #pragma unroll
@@ -771,7 +739,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     sum = group_fsum1(c, sum);
     const float pmean = __fdiv_rn(sum, (float)cnt);
     // ---- Phase 2 over the sample (Eq. 6)
-    const float mu = __fdiv_rn((float)(k * P2_S), (float)p.n);
+    const float mu = __fdiv_rn((float)(k * P2_S), (float)n);
     const int L = min(max((int)ceilf(__fadd_rn(mu, __fmul_rn(prm.window_z, __fsqrt_rn(mu)))), 1), P2_S);
     const int H = min(L + (L + 1) / 2, P2_S);
     const float ft = __fmul_rn((float)(L + H), 0.5f);
@@ -850,6 +818,52 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
     g.scount = (int32_t)hits;
     return g;
 }
+
+template <class G>
+__device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t (&gi)[GUESS_PER_THREAD], int k,
+                                            const GvrParams& prm, int32_t* sh256)
+{
+    static_assert(G::N == 256, "one sample chunk per thread");
+    constexpr int GPT = GUESS_PER_THREAD;  // 8 guessed positions per thread
+    if (p.n <= GVR_CAP) {  // the whole row fits in B: collect everything, no search
+        GuessOut g;
+        g.Tc = 0u;
+        g.tie = 0u;
+        g.T0 = 0u;
+        g.tmin = 0u;
+        g.top = 0xffffffffu;
+        g.t0_ok = 0;
+        g.iters = 0;
+        g.exit = GVR_P2_ALL;
+        g.scount = 0;
+        return g;
+    }
+    // ---- loads: the sample chunk, then the guessed values
+    const int nch = p.nfl / P2_CHUNK;  // >= 376 for n > GVR_CAP
+    const float4* sp4 =
+        reinterpret_cast<const float4*>(p.x + p.head + P2_CHUNK * (int)(((int64_t)c.tid * nch) >> 8));
+    float sv[P2_CHUNK];
+#pragma unroll
+    for (int q = 0; q < P2_CHUNK / 4; ++q) {
+        const float4 v = ldg_sample(sp4 + q);
+        sv[4 * q] = v.x;
+        sv[4 * q + 1] = v.y;
+        sv[4 * q + 2] = v.z;
+        sv[4 * q + 3] = v.w;
+    }
+    float gv[GPT];
+    uint32_t valid = 0;
+#pragma unroll
+    for (int j = 0; j < GPT; ++j) {
+        gv[j] = 0.f;
+        if (gi[j] >= 0 && gi[j] < p.n) {
+            gv[j] = ld_gather(p.x + gi[j]);
+            valid |= 1u << j;
+        }
+    }
+    return phase12_core(c, p.n, gv, valid, sv, k, prm, sh256);
+}
+
 
 // ---------------- Phases 1-2 for the batch paths
 // One 256-thread CTA per row, all rows resident at once: with every row's gathers in

@@ -11,6 +11,7 @@
 #include "refine_kernel.cuh"
 #include "radix_kernel.cuh"
 #include "radix2_kernel.cuh"
+#include "indexer_kernel.cuh"
 
 namespace {
 
@@ -462,7 +463,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         if (e == cudaSuccess)
             e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, scores,
                        row_stride, row_lens, (int)k,
-                       (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts);
+                       (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts, false);
         if (e == cudaSuccess)
             e = launch(gvr_fixup_kernel, min((int)num_rows, 2 * sms), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
                        (int)k, out_idx, out_val, stats, prm, gpc, prev_topk, phase_ts, ctl, bq);
@@ -530,6 +531,130 @@ gvr_status radix_topk_batched_ex(const float* scores, int64_t row_stride, const 
     radix_topk_kernel<<<num_rows, RADIX_NT, RADIX_SMEM_BYTES, stream>>>(scores, row_stride, row_lens, k, out_idx, out_val,
                                                             stats);
     return launch_status();
+}
+
+gvr_status gvr_indexer_scores(const void* keys, int64_t n_max, const int32_t* row_set, const int32_t* row_lens,
+                              const void* q, const float* w, int32_t num_rows, float* out, int64_t out_stride,
+                              cudaStream_t stream)
+{
+    if (num_rows < 0 || n_max < 1 || out_stride < n_max) return GVR_ERR_INVALID_ARGUMENT;
+    if (num_rows == 0) return GVR_OK;
+    if (!keys || !row_set || !q || !w || !out) return GVR_ERR_INVALID_ARGUMENT;
+    if (n_max > 0x7fffffffLL) return GVR_ERR_UNSUPPORTED;
+    gvr_status st;
+    if ((st = set_smem(indexer_scores_kernel, IX_SMEM_BYTES)) != GVR_OK) return st;
+    const IndexerArgs ia{static_cast<const __nv_bfloat16*>(keys), n_max, row_set, static_cast<const __nv_bfloat16*>(q), w};
+    const int tiles = (int)((n_max + IX_TILE - 1) / IX_TILE);
+    const dim3 grid((unsigned)min(tiles, 64), (unsigned)num_rows);
+    indexer_scores_kernel<<<grid, IX_NT, IX_SMEM_BYTES, stream>>>(ia, row_lens, out, out_stride);
+    return launch_status();
+}
+
+gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32_t* row_set, const int32_t* row_lens,
+                                    const void* q, const float* w, int32_t num_rows, const int32_t* prev_topk, int32_t k,
+                                    int32_t* out_idx, float* score_scratch, cudaStream_t stream)
+{
+    gvr_status st = validate(score_scratch, n_max, num_rows, k, out_idx);
+    if (st != GVR_OK) return st;
+    if (num_rows == 0) return GVR_OK;
+    if (!keys || !row_set || !q || !w) return GVR_ERR_INVALID_ARGUMENT;
+    if (n_max % 4 != 0 || (reinterpret_cast<uintptr_t>(score_scratch) & 15u) != 0) return GVR_ERR_UNSUPPORTED;
+    const size_t bytes = (size_t)num_rows * (size_t)k * sizeof(int32_t);
+    if (prev_topk && prev_topk != out_idx && ranges_overlap(prev_topk, bytes, out_idx, bytes))
+        return GVR_ERR_INVALID_ARGUMENT;
+    GvrParams prm;
+    prm.window_z = P2_Z_DEFAULT;
+    prm.max_secant = 8;
+    prm.guess_stride = GVR_DEFAULT_GUESS_STRIDE;
+    int sms = 0, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                   cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    if ((st = set_smem(indexer_guess_kernel, IXG_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(indexer_filter_kernel, IXF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(gvr_refine_kernel, RF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(indexer_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK)
+        return st;
+    // the candidate lists of the batch filter path, one filter CTA per SM
+    CandLists cl{};
+    const int tpr = (int)((n_max + STAGE_FLOATS - 1) / STAGE_FLOATS);
+    const long long V = (long long)num_rows * tpr;
+    const int min_tiles = (tpr + 2) / 3;
+    long long G = sms;
+    if (G > V / min_tiles) G = V / min_tiles;
+    if (G < 1) G = 1;
+    const long long per = (V + G - 1) / G;
+    long long reg = per * STAGE_FLOATS / 8;
+    if (reg < F_REG_MIN) reg = F_REG_MIN;
+    if (G * reg > 0x7fffffffLL) return GVR_ERR_UNSUPPORTED;
+    cl.V = V;
+    cl.G = (int)G;
+    cl.tpr = tpr;
+    cl.reg = (int)reg;
+    const size_t gp_bytes = (size_t)num_rows * sizeof(GuessOut);
+    const size_t fix_off = gp_bytes + (size_t)num_rows * 4;
+    const size_t rec_off = (fix_off + (size_t)num_rows * 4 + 255) & ~(size_t)255;
+    const size_t region_off = (rec_off + (size_t)num_rows * F_SEGS * sizeof(int4) + 255) & ~(size_t)255;
+    const size_t after_bytes = region_off + (size_t)G * (size_t)reg * sizeof(uint2);
+    ScratchLease lease;
+    if (acquire_scratch(stream, num_rows, [&](int64_t) { return after_bytes; }, lease) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    unsigned char* scratch = lease.ptr;
+    unsigned char* per_call = scratch + zero_region_bytes(lease.rows_cap);
+    int32_t* ctl = reinterpret_cast<int32_t*>(scratch);
+    GuessOut* gp = reinterpret_cast<GuessOut*>(per_call);
+    BatchQueue bq{};
+    bq.qctl = reinterpret_cast<int32_t*>(scratch + 16);
+    bq.queue = bq.qctl + 4;
+    bq.segdone = bq.queue + lease.rows_cap;
+    bq.fixlist = reinterpret_cast<int32_t*>(per_call + fix_off);
+    cl.rec = reinterpret_cast<int4*>(per_call + rec_off);
+    cl.region = reinterpret_cast<uint2*>(per_call + region_off);
+    cudaError_t e = cudaSuccess;
+    if (lease.fresh) e = cudaMemsetAsync(scratch, 0, zero_region_bytes(lease.rows_cap), stream);
+    const IndexerArgs ia{static_cast<const __nv_bfloat16*>(keys), n_max, row_set, static_cast<const __nv_bfloat16*>(q), w};
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    auto launch = [&](auto kern, int grid, int threads, int smem_bytes, auto... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.dynamicSmemBytes = (size_t)smem_bytes;
+        cfg.stream = stream;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, args...);
+    };
+    const float* sc = score_scratch;
+    const GuessOut* gpc = gp;
+    if (e == cudaSuccess)
+        e = launch(indexer_guess_kernel, (int)num_rows, IX_NT, IXG_SMEM_BYTES, ia, sc, row_lens, prev_topk, (int)k, prm,
+                   gp, bq);
+    if (e == cudaSuccess)
+        e = launch(indexer_filter_kernel, cl.G, IX_NT, IXF_SMEM_BYTES, ia, sc, row_lens, (int)k, gpc, cl, bq);
+    if (e == cudaSuccess)
+        e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, sc, n_max,
+                   row_lens, (int)k, (int)num_rows, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, gpc, cl, bq,
+                   (long long*)nullptr, true);
+    if (e == cudaSuccess)
+        e = launch(indexer_fixup_kernel, min((int)num_rows, sms), GVR_NT, GVR_SMEM_BYTES, ia, score_scratch, row_lens,
+                   (int)k, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, prm, gpc, prev_topk, ctl, bq);
+    if (e != cudaSuccess) {
+        g_last_cuda_error = e;
+        (void)cudaGetLastError();
+        lease.fail();
+    }
+    const gvr_status ls = e != cudaSuccess ? GVR_ERR_CUDA : launch_status();
+    if (lease.temporary && cudaFreeAsync(scratch, stream) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    return ls;
 }
 
 gvr_status radix2_topk_batched_ex(const float* scores, int64_t row_stride, const int32_t* row_lens,

@@ -78,8 +78,10 @@ __device__ __forceinline__ void for_list(const RefineGroup& c, const CandLists& 
 __global__ void __launch_bounds__(RF_NT, RF_CTAS_PER_SM)
 gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   int num_rows, int32_t* out, float* out_val, gvr_row_stats* stats, const GuessOut* gp, CandLists cl,
-                  BatchQueue bq, long long* phase_ts)
+                  BatchQueue bq, long long* phase_ts, bool fused = false)
 {
+    // fused (the indexer path, indexer_kernel.cuh): the score rows do not exist, so rows
+    // that need them — len <= k, the ties fill — go to the fixup list, which materialises them
     // phase_ts (optional, [num_rows][TS_N]): clock64 at the pop, after the segment records,
     // after the histogram pass, after the K-th bin search, after the scatter, at the end;
     // then globaltimer at the pop and the end, and the SM id.
@@ -171,13 +173,14 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         const int p2exit = (int)(int16_t)(g1.y >> 16);
         const bool tie_fill = p.ntiles > 0 && p.n > k && p2exit == GVR_P2_TIES && tie < 0xffffffffu &&
                               Tc == tie + 1u && total >= 0 && total < K;
-        if (tie_fill) ok = total == 0 || kmax >= Tc;
+        if (tie_fill) ok = !fused && (total == 0 || kmax >= Tc);
         // a row with len <= k: every element is selected (take = len), binned over its own
         // key range [min, max], then -1 padding (R5)
         const bool trivial = p.n <= k;
         const float* rowx = nullptr;
         int take = tie_fill ? total : K;
-        if (trivial) {
+        if (trivial && fused) ok = false;
+        if (trivial && !fused) {
             uint32_t mn = 0xffffffffu, mx2 = 0u;
             for (int q = c.tid; q < p.n; q += RF_NT) {
                 const uint32_t kv = f2key(__ldg(p.x + q));
@@ -354,7 +357,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             levels = 0;
             ftc = total;
         }
-        if (trivial && p.n == 0) {
+        if (trivial && p.n == 0 && !fused) {
             int32_t* o = out + (int64_t)r * k;
             for (int j = c.tid; j < k; j += RF_NT) {
                 o[j] = -1;

@@ -134,6 +134,14 @@ class IndexerLayer:
         self.q = r * self.q + s * torch.randn(self.heads, self.dim, generator=self._g, device=self.device)
         self.w = r * self.w + s * torch.randn(self.heads, generator=self._g, device=self.device) / math.sqrt(self.heads)
 
+    def query(self, n: int) -> torch.Tensor:
+        """The step's indexer query Q_t [heads, dim], RoPE'd at the newest position n - 1."""
+        q = self.q.clone()
+        q[:, :self.d_rope] = rope_rotate(q[:, :self.d_rope],
+                                         torch.full((self.heads,), n - 1, device=self.device),
+                                         self.inv_freq)
+        return q
+
     def scores(self, n: int) -> torch.Tensor:
         """Eq. 1 score row over the first n keys for the current query state (fp32)."""
         assert 0 < n <= self.n_max

@@ -293,3 +293,73 @@ def test_fixup_kernel_short_lists(gvr):
     got, st = _run(gvr, s, lens, prev, opts=gvr.GvrOptions(-8.0, 0, 0, 0, 0))
     _assert_exact(got, oracle.topk_batched(s.cpu().numpy(), K), st)
     assert (_col(st, "global_passes") == 2).all(), st[:3].tolist()
+
+
+# ------------------------------------------------------------------ indexer (f3)
+def _indexer_inputs(sets, rows_per_set, n, seed, rho=0.9):
+    """bf16 key sets from the Eq.-1 generator (RoPE'd keys) and per-row bf16 queries / fp32
+    weights: row j of set s is the query of draft j (one more AR step each)."""
+    import torch
+    dev = torch.device("cuda:0")
+    keys, qs, ws, row_set, lay_prev = [], [], [], [], []
+    for si in range(sets):
+        lay = synth.IndexerLayer(n, rho, synth.splitmix64(seed, si), dev)
+        keys.append(lay.keys[:n].to(torch.bfloat16))
+        for j in range(rows_per_set):
+            if j:
+                lay.step()
+            qs.append(lay.query(n).to(torch.bfloat16))
+            ws.append(lay.w.clone())
+            row_set.append(si)
+    return (torch.stack(keys).contiguous(), torch.tensor(row_set, dtype=torch.int32, device=dev),
+            torch.stack(qs).contiguous(), torch.stack(ws).float().contiguous())
+
+
+def test_indexer_scores_match_eq1(gvr):
+    """Tensor-core indexer scores (bf16 inputs, fp32 accumulation) equal Eq. 1 evaluated in
+    fp64 from the same bf16 inputs within the fp32 rounding bound; ragged lengths."""
+    import torch
+    from oracle import indexer as IX
+    keys, row_set, q, w = _indexer_inputs(2, 3, 5_000, seed=3200)
+    lens = torch.tensor([5_000, 4_999, 77, 4_096, 1, 3_333], dtype=torch.int32, device="cuda:0")
+    out = gvr.indexer_scores(keys, row_set, q, w, row_lens=lens)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    kh, qh, wh = keys.float().cpu().numpy(), q.float().cpu().numpy(), w.cpu().numpy()
+    for r in range(6):
+        n = int(lens[r])
+        s64 = IX.scores64(kh[int(row_set[r]), :n], qh[r], wh[r])
+        eps = IX.score_error_bound(kh[int(row_set[r]), :n], qh[r], wh[r])
+        assert (np.abs(o[r, :n] - s64) <= eps).all(), (r, float(np.abs(o[r, :n] - s64).max()), float(eps.min()))
+        assert (o[r, n:] == 0).all()
+
+
+@pytest.mark.parametrize("sets,rows_per_set,n", [(4, 1, 20_000), (80, 4, 9_000), (3, 2, 100_000)])
+def test_indexer_topk_fused(gvr, sets, rows_per_set, n):
+    """Fused indexer -> Top-K (f3): (a) bit-identical to the unfused path (the same scores
+    materialised by gvr_indexer_scores, then gvr_topk_batched) — fusion changes nothing;
+    (b) a valid ordered Top-K of Eq. 1 evaluated in fp64 from the same bf16 inputs, within
+    the fp32 rounding bound.  Batches of one wave and of more (the filter path), MTP rows
+    sharing a key set, ragged lengths including a row of <= k keys."""
+    import torch
+    from oracle import indexer as IX
+    keys, row_set, q, w = _indexer_inputs(sets, rows_per_set, n, seed=3300 + n)
+    R = row_set.shape[0]
+    rng = np.random.default_rng(3301)
+    lens_np = rng.integers(n // 2, n + 1, size=R).astype(np.int32)
+    lens_np[0] = n
+    if R > 2:
+        lens_np[1] = 1500  # <= k: materialised by the fixup
+    lens = torch.from_numpy(lens_np).cuda()
+    prev = torch.from_numpy(np.stack([rng.integers(0, n, K) for _ in range(R)]).astype(np.int32)).cuda()
+    fused = gvr.indexer_topk(keys, row_set, q, w, K, row_lens=lens, prev=prev)
+    sc = gvr.indexer_scores(keys, row_set, q, w, row_lens=lens)
+    unfused = gvr.topk(sc, K, row_lens=lens, prev=prev)
+    torch.cuda.synchronize()
+    fo, uo = fused.cpu().numpy(), unfused.cpu().numpy()
+    _assert_exact(fo, uo)
+    kh, qh, wh = keys.float().cpu().numpy(), q.float().cpu().numpy(), w.cpu().numpy()
+    for r in range(0, R, max(1, R // 6)):
+        m = int(lens_np[r])
+        kk = kh[int(row_set[r]), :m]
+        IX.check_topk_within(fo[r], IX.scores64(kk, qh[r], wh[r]), IX.score_error_bound(kk, qh[r], wh[r]), K)
