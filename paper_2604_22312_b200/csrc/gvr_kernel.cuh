@@ -124,7 +124,8 @@ __host__ __device__ __forceinline__ int cl_cta_of(const CandLists& cl, long long
 // CTA finishing a row's last segment pushes it; gvr_guess_kernel pushes rows with no
 // tiles); gvr_refine_kernel pops them in that order and appends the rows it cannot
 // finish to the fixup list, which gvr_topk_kernel (fixup mode) works off last.
-enum { Q_HEAD = 0, Q_TAIL = 1, Q_NFIX = 2, Q_WORDS = 4 };
+enum { Q_HEAD = 0, Q_TAIL = 1, Q_NFIX = 2, Q_RDONE = 3, Q_WORDS = 4 };
+constexpr int CTL_RDONE = 3;  // ctl word: set (release) by the last refine CTA to finish
 struct BatchQueue {
     int32_t* qctl;     // [Q_WORDS]
     int32_t* queue;    // [num_rows]: row + 1 once pushed, reset to 0 when popped
@@ -925,9 +926,22 @@ __device__ __forceinline__ void fixup_done(int32_t* ctl, const BatchQueue& bq, i
         ctl[0] = 0;
         ctl[1] = 0;
         ctl[2] = 0;
+        ctl[CTL_RDONE] = 0;
         if (bq.qctl)
             for (int i = 0; i < Q_WORDS; ++i) bq.qctl[i] = 0;
     }
+}
+
+// The fixup kernels' start: thread 0 waits for the last refine CTA's release flag.
+__device__ __forceinline__ void fixup_wait(int32_t* ctl)
+{
+    __shared__ int go;
+    if (threadIdx.x == 0) {
+        while (ld_acquire(ctl + CTL_RDONE) == 0) __nanosleep(128);
+        go = 1;
+    }
+    __syncthreads();
+    (void)go;
 }
 
 // One row, the whole path: Phases 1-2 (or their hand-off), the streaming pass, Phases 3-4
@@ -1119,7 +1133,10 @@ gvr_fixup_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
                  int32_t* out, float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
                  const int32_t* prev, long long* phase_ts, int32_t* ctl, BatchQueue bq)
 {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the refine grid's fixup list is complete
+    // The refine grid's fixup list is complete once its last CTA sets the flag (this grid
+    // is launched only after every refine CTA has started, so spinning cannot starve it);
+    // an empty list lets the CTAs leave before the refine grid has even retired.
+    fixup_wait(ctl);
     const int nfix = ld_relaxed(bq.qctl + Q_NFIX);
     uint32_t pbits = 0u;  // stage phase parities carried across this CTA's rows
     for (int li = (int)blockIdx.x; li < nfix; li += (int)gridDim.x)

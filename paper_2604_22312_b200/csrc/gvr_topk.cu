@@ -463,7 +463,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         if (e == cudaSuccess)
             e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, scores,
                        row_stride, row_lens, (int)k,
-                       (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts, false);
+                       (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts, false, ctl);
         if (e == cudaSuccess)
             e = launch(gvr_fixup_kernel, min((int)num_rows, 2 * sms), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
                        (int)k, out_idx, out_val, stats, prm, gpc, prev_topk, phase_ts, ctl, bq);
@@ -640,7 +640,7 @@ gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32
     if (e == cudaSuccess)
         e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, sc, n_max,
                    row_lens, (int)k, (int)num_rows, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, gpc, cl, bq,
-                   (long long*)nullptr, true);
+                   (long long*)nullptr, true, ctl);
     if (e == cudaSuccess)
         e = launch(indexer_fixup_kernel, min((int)num_rows, sms), GVR_NT, GVR_SMEM_BYTES, ia, score_scratch, row_lens,
                    (int)k, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, prm, gpc, prev_topk, ctl, bq);

@@ -502,7 +502,7 @@ indexer_fixup_kernel(IndexerArgs ia, float* scratch, const int32_t* __restrict__
                      float* out_val, gvr_row_stats* stats, GvrParams prm, const GuessOut* __restrict__ gp,
                      const int32_t* prev, int32_t* ctl, BatchQueue bq)
 {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the refine grid's fixup list is complete
+    fixup_wait(ctl);  // the refine grid's fixup list is complete
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t sbase = smem_u32(smem);
     // materialisation area (inside the row kernel's layout; idle between rows)

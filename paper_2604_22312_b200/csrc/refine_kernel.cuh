@@ -1,7 +1,7 @@
 // refine_kernel.cuh — the batch path's refine step: Phase 4 and the ordered output from the
 // candidate lists gvr_filter_kernel leaves in L2.
 //
-// A persistent grid of four small CTAs per SM (29 KB of shared memory, <= 64 registers)
+// A persistent grid of four small CTAs per SM (37 KB of shared memory, <= 64 registers)
 // launched behind the filter with programmatic dependent launch: one wave covers a decode
 // batch, and CTAs that find room early start on the rows already complete.  CTAs pop rows
 // from the ready queue in the // order their lists complete.  Per row (all of it exact key-space arithmetic):
@@ -24,31 +24,25 @@ namespace gvr {
 
 constexpr int RF_NT = 256;
 constexpr int RF_CSORT = 2560;     // entries up to the K-th bin sorted in shared memory
-constexpr int RF_MAXLIST = 65535;  // bin counts and cursors are 16-bit
+constexpr int RF_MAXLIST = 1 << 22;  // longest list refined here
 constexpr int RF_BIN_FAST = 16;    // largest bin ranked without narrowing first
 using RefineGroup = Group<RF_NT, 1>;
-constexpr int RF_OFF_HIST = 0;                       // u16 bin counts, two per word
-constexpr int RF_OFF_CUR = RF_OFF_HIST + NBINS * 2;  // u16 bin cursors, two per word
-constexpr int RF_OFF_CS = RF_OFF_CUR + NBINS * 2;
+constexpr int RF_OFF_HIST = 0;                       // int32 bin counts
+constexpr int RF_OFF_CUR = RF_OFF_HIST + NBINS * 4;  // int32 bin cursors
+constexpr int RF_OFF_CS = RF_OFF_CUR + NBINS * 4;
 constexpr int RF_OFF_ROW = RF_OFF_CS + RF_CSORT * 8;
 constexpr int RF_OFF_SCR = RF_OFF_ROW + 16;
 constexpr int RF_SMEM_BYTES = RF_OFF_SCR + GROUP_SCRATCH_BYTES;
 constexpr int RF_CTAS_PER_SM = 4;  // one wave for a decode batch: the per-row work is latency bound
 static_assert(RF_CTAS_PER_SM * (RF_SMEM_BYTES + 1024) <= 233472, "refine CTAs per SM");
 
-// 16-bit counters packed two per 32-bit word (shared memory)
-__device__ __forceinline__ int h16_get(const uint32_t* w, int b) { return (int)((w[b >> 1] >> ((b & 1) * 16)) & 0xffffu); }
-__device__ __forceinline__ int h16_add(uint32_t* w, int b)
-{
-    const int sh = (b & 1) * 16;
-    return (int)((atomicAdd(&w[b >> 1], 1u << sh) >> sh) & 0xffffu);
-}
 
 // Visit the row's list in batches of UNR entries per thread, segment by segment (segment s:
 // n[s] entries from region position gs[s]; a row with len <= k is one segment read from
-// the row itself, rowx).  fn(kv, pos, valid) gets the keys, the entries' region positions
-// (or row positions) and a validity mask.
-template <int UNR, class Fn>
+// the row itself, rowx).  fn(kv, aux, valid) gets the keys, a validity mask and per entry
+// either its region position (or row position) or, WITH_IDX, its row index (the entry's
+// second word, loaded with the key).
+template <int UNR, bool WITH_IDX = false, class Fn>
 __device__ __forceinline__ void for_list(const RefineGroup& c, const CandLists& cl, const float* rowx,
                                          const int (&gs)[F_SEGS], const int (&n)[F_SEGS], Fn&& fn)
 {
@@ -58,19 +52,28 @@ __device__ __forceinline__ void for_list(const RefineGroup& c, const CandLists& 
         const int base = gs[s], ns = n[s];
         for (int j0 = c.tid; j0 < ns; j0 += UNR * RF_NT) {
             uint32_t kv[UNR];
-            int pos[UNR];
+            int aux[UNR];
             uint32_t valid = 0u;
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const int j = j0 + u * RF_NT;
-                pos[u] = base + j;
+                const int pos = base + j;
                 kv[u] = 0u;
+                aux[u] = pos;
                 if (j < ns) {
-                    kv[u] = rowx ? f2key(__ldg(rowx + pos[u])) : __ldcg(rk + 2 * (size_t)pos[u]);
+                    if (rowx) {
+                        kv[u] = f2key(__ldg(rowx + pos));
+                    } else if (WITH_IDX) {
+                        const uint2 e = __ldcg(cl.region + pos);
+                        kv[u] = e.x;
+                        aux[u] = (int)e.y;
+                    } else {
+                        kv[u] = __ldcg(rk + 2 * (size_t)pos);
+                    }
                     valid |= 1u << u;
                 }
             }
-            fn(kv, pos, valid);
+            fn(kv, aux, valid);
         }
     }
 }
@@ -78,16 +81,18 @@ __device__ __forceinline__ void for_list(const RefineGroup& c, const CandLists& 
 __global__ void __launch_bounds__(RF_NT, RF_CTAS_PER_SM)
 gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   int num_rows, int32_t* out, float* out_val, gvr_row_stats* stats, const GuessOut* gp, CandLists cl,
-                  BatchQueue bq, long long* phase_ts, bool fused = false)
+                  BatchQueue bq, long long* phase_ts, bool fused = false, int32_t* ctl = nullptr)
 {
+    // the fixup grid may be scheduled now: it waits for this grid's release flag (ctl)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // fused (the indexer path, indexer_kernel.cuh): the score rows do not exist, so rows
     // that need them — len <= k, the ties fill — go to the fixup list, which materialises them
     // phase_ts (optional, [num_rows][TS_N]): clock64 at the pop, after the segment records,
     // after the histogram pass, after the K-th bin search, after the scatter, at the end;
     // then globaltimer at the pop and the end, and the SM id.
     extern __shared__ __align__(128) unsigned char smem[];
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + RF_OFF_HIST);
-    uint32_t* cur = reinterpret_cast<uint32_t*>(smem + RF_OFF_CUR);
+    int32_t* hist = reinterpret_cast<int32_t*>(smem + RF_OFF_HIST);
+    int32_t* cur = reinterpret_cast<int32_t*>(smem + RF_OFF_CUR);
     unsigned long long* cs = reinterpret_cast<unsigned long long*>(smem + RF_OFF_CS);
     int* sh_row = reinterpret_cast<int*>(smem + RF_OFF_ROW);
     RefineGroup c;
@@ -214,7 +219,8 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             int bk = -1;
             for (int lvl = 0; lvl < 3; ++lvl) {
                 levels = lvl + 1;
-                for (int i = c.tid; i < NBINS / 2; i += RF_NT) hist[i] = 0u;
+                reinterpret_cast<int4*>(hist + b0)[0] = make_int4(0, 0, 0, 0);
+                reinterpret_cast<int4*>(hist + b0)[1] = make_int4(0, 0, 0, 0);
                 if (c.tid == 0) c.misc[12] = -1;  // K-th bin: set below by the thread that holds it
                 c.sync();
                 scale = bin_scale((uint64_t)kmax - lo + 1ull);
@@ -223,7 +229,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
                         if ((valid >> u & 1u) && kv[u] >= lo) {
-                            h16_add(hist, (NBINS - 1) - lin_bin(kv[u] - lo, scale));
+                            atomicAdd(&hist[(NBINS - 1) - lin_bin(kv[u] - lo, scale)], 1);
                             ++f;
                         }
                 });
@@ -233,11 +239,14 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                     if (phase_ts) tsr[TS_STREAM] = clock64();
                 }
                 uint32_t loc = 0;
-#pragma unroll
-                for (int i = 0; i < BPT; ++i) {
-                    h[i] = h16_get(hist, b0 + i);
-                    loc += (uint32_t)h[i];
+                {
+                    const int4 h0 = reinterpret_cast<const int4*>(hist + b0)[0];
+                    const int4 h1 = reinterpret_cast<const int4*>(hist + b0)[1];
+                    h[0] = h0.x, h[1] = h0.y, h[2] = h0.z, h[3] = h0.w;
+                    h[4] = h1.x, h[5] = h1.y, h[6] = h1.z, h[7] = h1.w;
                 }
+#pragma unroll
+                for (int i = 0; i < BPT; ++i) loc += (uint32_t)h[i];
                 uint32_t tot;
                 off0 = group_excl_scan(c, loc, tot);
                 {
@@ -271,26 +280,25 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             if (phase_ts) tsr[TS_PHASE23] = clock64();
             if (ok) {
                 {
-                    uint32_t off = off0;
+                    // bin starts; they become the bin ends after the scatter
+                    int st[BPT];
+                    int off = (int)off0;
 #pragma unroll
-                    for (int i = 0; i < BPT; i += 2) {
-                        // bin starts (two per word); they become the bin ends after the scatter
-                        cur[(b0 + i) >> 1] = off | ((off + (uint32_t)h[i]) << 16);
-                        off += (uint32_t)h[i] + (uint32_t)h[i + 1];
+                    for (int i = 0; i < BPT; ++i) {
+                        st[i] = off;
+                        off += h[i];
                     }
+                    reinterpret_cast<int4*>(cur + b0)[0] = make_int4(st[0], st[1], st[2], st[3]);
+                    reinterpret_cast<int4*>(cur + b0)[1] = make_int4(st[4], st[5], st[6], st[7]);
                 }
                 c.sync();
                 // ---- counting sort of the bins up to the K-th bin (composites)
-                for_list<UNR>(c, cl, rowx, gs, ns, [&](const uint32_t (&kv)[UNR], const int (&pos)[UNR], uint32_t valid) {
-                    int b[UNR], ix[UNR];
+                for_list<UNR, true>(c, cl, rowx, gs, ns, [&](const uint32_t (&kv)[UNR], const int (&ix)[UNR], uint32_t valid) {
 #pragma unroll
                     for (int u = 0; u < UNR; ++u) {
-                        b[u] = (valid >> u & 1u) && kv[u] >= lo ? (NBINS - 1) - lin_bin(kv[u] - lo, scale) : NBINS;
-                        ix[u] = b[u] <= bk ? (rowx ? pos[u] : __ldcg(cl.region + pos[u]).y) : 0;
+                        const int b = (valid >> u & 1u) && kv[u] >= lo ? (NBINS - 1) - lin_bin(kv[u] - lo, scale) : NBINS;
+                        if (b <= bk) cs[atomicAdd(&cur[b], 1)] = make_comp(kv[u], ix[u]);
                     }
-#pragma unroll
-                    for (int u = 0; u < UNR; ++u)
-                        if (b[u] <= bk) cs[h16_add(cur, b[u])] = make_comp(kv[u], ix[u]);
                 });
                 c.sync();
                 if (phase_ts) tsr[TS_PHASE4] = clock64();
@@ -301,8 +309,8 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 for (int j = c.tid; j < nsel; j += RF_NT) {
                     const unsigned long long v = cs[j];
                     const int b = (NBINS - 1) - lin_bin(comp_key(v) - lo, scale);
-                    const int cnt = h16_get(hist, b);
-                    const int st = h16_get(cur, b) - cnt;
+                    const int cnt = hist[b];
+                    const int st = cur[b] - cnt;
                     const int wmax = (int)__reduce_max_sync(__activemask(), (uint32_t)cnt);
                     int rank = 0;
                     if (wmax <= 4) {
@@ -396,6 +404,14 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             }
         }
         c.sync();  // smem (row slot, histogram, sort buffer) is reused for the next row
+    }
+    // the last CTA to finish releases the fixup grid (its list is complete)
+    if (c.tid == 0 && ctl) {
+        __threadfence();
+        if (atomicAdd(bq.qctl + Q_RDONE, 1) == (int)gridDim.x - 1) {
+            __threadfence();
+            st_release(ctl + CTL_RDONE, 1);
+        }
     }
 }
 
