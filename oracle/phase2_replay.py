@@ -162,7 +162,8 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
     bracket end on the far side of the window.  Exits: DONE_WINDOW (T_c = T), DONE_TIES
     (adjacent anchors: no key in the window — a tie group spans it; T_c = the lo anchor,
     whose count is above the window), DONE_EXHAUSTED (MAX_ITERS probes; T_c = the sample
-    key of rank ceil(f_t), the exact finisher over the sample).
+    key of rank ceil(f_t), the exact finisher over the sample — DONE_TIES instead when that
+    key's count is above the window: its tie group spans the window, R37).
     Returns (T_c key, I = probes, done, count at T_c)."""
     L, H, ft = window(n, k, z)
     sk = np.asarray(sample_keys, dtype=np.uint32)
@@ -205,7 +206,9 @@ def phase2(sample_keys: np.ndarray, p1, n: int, k: int, z=Z, max_secant: int = M
             # the exact finisher over the sample (R12): the key of rank ceil(f_t)
             rank = (L + H + 1) // 2
             T = int(np.sort(sk)[::-1][rank - 1])
-            return T, it, DONE_EXHAUSTED, int(np.count_nonzero(sk >= np.uint32(T)))
+            c = int(np.count_nonzero(sk >= np.uint32(T)))
+            # a key whose tie group reaches past the window: a ties exit at it (R37)
+            return T, it, DONE_TIES if c > H else DONE_EXHAUSTED, c
         T = secant_step(klo, clo, khi, chi, ft, first_secant, secants >= max_secant)
         first_secant = False
         secants += 1

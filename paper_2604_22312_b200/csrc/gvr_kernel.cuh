@@ -802,6 +802,11 @@ __device__ __forceinline__ GuessOut phase12_core(G& c, int n, const float (&gv)[
 #pragma unroll
         for (int q = 0; q < P2_CHUNK; ++q) m += sk[q] >= T ? 1u : 0u;
         hits = group_red1<R_ADD>(c, m);
+        if (hits > (uint32_t)H) {
+            // that key is a tie group reaching past the window (R37): a ties exit at it
+            exitk = GVR_P2_TIES;
+            g.tie = T;
+        }
     } else if (!found) {
         // ties: the anchors are adjacent keys — the lo anchor's key holds a tie group that
         // spans the window (its hits are above it, the next key's below)

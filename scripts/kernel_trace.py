@@ -8,11 +8,30 @@ import paper_2604_22312_b200 as gvr
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--impl", default="gvr")
+ap.add_argument("--case", default=None, help="worst_cases.py batch kind:guess, e.g. ties90:random")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 dev = torch.device("cuda:0")
-bs = [bench.make_decode_batch(cfg["requests"], cfg["layers"], cfg["n"], dev, seed=synth.splitmix64(synth.BASE_SEED, i),
-                              draft=cfg["draft"]) for i in range(3)]
+if args.case:
+    import numpy as np
+    kind, gk = args.case.split(":")
+    R, N = 488, 100_000
+    def dist_batch(seed):
+        s = torch.from_numpy(np.stack([synth.dist_row(kind, N, seed=seed + r) for r in range(R)])).to(dev)
+        if gk == "adversarial":
+            prev = torch.argsort(s, dim=1, stable=True)[:, :bench.K].to(torch.int32).contiguous()
+        else:
+            prev = torch.randint(0, N, (R, bench.K), dtype=torch.int32, device=dev,
+                                 generator=torch.Generator(dev).manual_seed(seed))
+        return {"scores": s, "row_lens": torch.full((R,), N, dtype=torch.int32, device=dev), "prev": prev, "R": R}
+    bs = [dist_batch(9000 + 1000 * i) for i in range(3)]
+    _, _, st = gvr.topk_ex(bs[0]["scores"], bench.K, row_lens=bs[0]["row_lens"], prev=bs[0]["prev"])
+    st = st.cpu().numpy()
+    for i, f in enumerate(gvr.STATS_FIELDS):
+        print(f"{f:14s} mean {st[:, i].mean():10.2f} min {st[:, i].min():10d} max {st[:, i].max():10d}")
+else:
+    bs = [bench.make_decode_batch(cfg["requests"], cfg["layers"], cfg["n"], dev, seed=synth.splitmix64(synth.BASE_SEED, i),
+                                  draft=cfg["draft"]) for i in range(3)]
 out = torch.empty((bs[0]["R"], bench.K), dtype=torch.int32, device=dev)
 it = [0]
 def step():

@@ -195,6 +195,27 @@ def test_massive_ties_batch_through_fixup(gvr):
     assert (_col(st, "done_kind") == 2).sum() > 0  # tie fill ran
 
 
+def test_ties90_exhausted_becomes_ties_exit(gvr):
+    """488 rows of N = 100K with 90% of the values tied at 0.25 (synth.dist_row ties90) on
+    the filter path: rows whose sample cannot reach the window end at the tie key; that
+    key's sample count is above the window, so the exit is a ties exit (R37) and the row is
+    collected strictly above the tie instead of taking the whole tie group into its list.
+    Phase-2 statistics equal the CPU replay row by row, no row needs the fixup, exact."""
+    import torch
+    R, n = 488, 100_000
+    host = np.stack([synth.dist_row("ties90", n, seed=9000 + r) for r in range(R)]).astype(np.float32)
+    lens = np.full(R, n, np.int32)
+    prev = np.stack([synth.guess("random", host[r], K, 9001 + r) for r in range(R)]).astype(np.int32)
+    dev = torch.device("cuda:0")
+    got, st = _run(gvr, torch.from_numpy(host).to(dev), torch.from_numpy(lens).to(dev), torch.from_numpy(prev).to(dev))
+    _assert_exact(got, oracle.topk_batched(host, K, row_lens=lens), st)
+    _assert_replay(host, lens, prev, st, filter_path=True, rows=range(0, R, 3))
+    assert (_col(st, "phase2_exit") == P2.DONE_TIES).sum() > 0
+    assert (_col(st, "phase2_exit") == P2.DONE_EXHAUSTED).sum() == 0
+    assert (_col(st, "global_passes") == 1).all()
+    assert (_col(st, "cand_count") < 8 * K).all()
+
+
 def test_snap_branch_runs(gvr):
     """A tie group of 300 at the row maximum crowds one bin above the K-th one, so the
     sorted-bin shortcut (R28) is refused and Phase 4's snap iterations
