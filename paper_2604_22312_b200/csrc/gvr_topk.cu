@@ -420,6 +420,11 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     static const bool no_pdl = getenv("GVR_NO_PDL") != nullptr;  // experiments: serialise the kernels
+    // fixup grid: one CTA per SM — the list is usually empty, and an empty fixup grid costs
+    // its CTAs' scheduling and drain after the refine (2 per SM: cfg2 +1 us; a batch that
+    // sends every row to the fixup takes ~2x longer at 1 per SM, still <= 2 passes per row)
+    static const int fixup_per_sm = getenv("GVR_FIXUP_PER_SM") ? atoi(getenv("GVR_FIXUP_PER_SM")) : 1;  // experiments
+    const int fixup_ctas = fixup_per_sm > 0 ? fixup_per_sm * sms : 16;
     pdl[0].val.programmaticStreamSerializationAllowed = (ev || no_pdl) ? 0 : 1;
     auto launch = [&](auto kern, int grid, int threads, int smem_bytes, auto... args) {
         cudaLaunchConfig_t cfg = {};
@@ -465,7 +470,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
                        row_stride, row_lens, (int)k,
                        (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts, false, ctl);
         if (e == cudaSuccess)
-            e = launch(gvr_fixup_kernel, min((int)num_rows, 2 * sms), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
+            e = launch(gvr_fixup_kernel, min((int)num_rows, fixup_ctas), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
                        (int)k, out_idx, out_val, stats, prm, gpc, prev_topk, phase_ts, ctl, bq);
     } else {
         e = launch(gvr_topk_kernel, (int)num_rows, GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens, (int)k, out_idx,
