@@ -108,6 +108,12 @@ __device__ __forceinline__ void issue_pair(const Ring& ring, const RoundIter& it
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ring.full(s0 + 1)) : "memory");
 }
 
+// Diagnostics (gvr_filter_cta_times): per filter CTA, globaltimer at entry, after the
+// Phase-1/2 wait and at exit, recorded while g_fts_on is set.
+constexpr int FTS_MAX = 4096;
+__device__ int g_fts_on;
+__device__ long long g_fts[FTS_MAX][4];
+
 __global__ void __launch_bounds__(F_NT, F_CTAS_PER_SM)
 gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   const GuessOut* __restrict__ gp, CandLists cl, BatchQueue bq)
@@ -120,6 +126,8 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     FilterGroup c;
     c.init(threadIdx.x, smem + F_OFF_SCR);
     const int b = blockIdx.x;
+    const bool fts = c.tid == 0 && b < FTS_MAX && *(volatile int*)&g_fts_on;
+    if (fts) g_fts[b][0] = global_ns();
     const long long vb = cl_begin(cl, b), ve = cl_begin(cl, b + 1);
     RoundIter prod;  // thread 0: two rounds ahead of the consumers
     prod.start(vb, ve, cl.tpr);
@@ -135,6 +143,7 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");  // gp (Phase 1) is complete and visible
+    if (fts) g_fts[b][1] = global_ns();
     c.sync();
     uint2* reg = cl.region + (long long)b * cl.reg;
     const int regcap = cl.reg;
@@ -242,6 +251,10 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             }
             c.sync();  // no reservation of the next segment before the cursor was read
         }
+    }
+    if (fts) {
+        g_fts[b][2] = global_ns();
+        g_fts[b][3] = sm_id();
     }
 }
 

@@ -223,6 +223,26 @@ const char* gvr_status_string(gvr_status s)
 
 int32_t gvr_version(void) { return kVersion; }
 
+gvr_status gvr_filter_cta_times(int32_t enable, int64_t* host_out, int32_t max_ctas, int32_t* n_out)
+{
+    const int on = enable ? 1 : 0;
+    if (!enable) {
+        if (!host_out || max_ctas < 0) return GVR_ERR_INVALID_ARGUMENT;
+        const int n = min((int)max_ctas, FTS_MAX);
+        if (cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpyFromSymbol(host_out, g_fts, (size_t)n * 4 * sizeof(long long)) != cudaSuccess) {
+            g_last_cuda_error = cudaGetLastError();
+            return GVR_ERR_CUDA;
+        }
+        if (n_out) *n_out = n;
+    }
+    if (cudaMemcpyToSymbol(g_fts_on, &on, sizeof(int)) != cudaSuccess) {
+        g_last_cuda_error = cudaGetLastError();
+        return GVR_ERR_CUDA;
+    }
+    return GVR_OK;
+}
+
 gvr_status gvr_kernel_info(int32_t* gvr_ctas_per_sm, int32_t* gvr_threads, int32_t* gvr_smem_bytes,
                            int32_t* radix_ctas_per_sm, int32_t* radix_threads, int32_t* radix_smem_bytes)
 {
@@ -386,7 +406,8 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     }
     if (radix2 && (st = set_smem(radix_hist_kernel, RH_SMEM_BYTES)) != GVR_OK) return st;
     if (filt && ((st = set_smem(gvr_filter_kernel, F_SMEM_BYTES)) != GVR_OK ||
-                 (st = set_smem(gvr_refine_kernel, RF_SMEM_BYTES)) != GVR_OK ||
+                 (st = set_smem(gvr_refine_kernel<false>, RF_SMEM_BYTES)) != GVR_OK ||
+                 (st = set_smem(gvr_refine_kernel<true>, RF_SMEM_BYTES)) != GVR_OK ||
                  (st = set_smem(gvr_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK))
         return st;
     ScratchLease lease;
@@ -466,7 +487,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         e = launch(gvr_filter_kernel, cl.G, F_NT, F_SMEM_BYTES, scores, row_stride, row_lens, (int)k, gpc, cl, bq);
         mark(2);
         if (e == cudaSuccess)
-            e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, scores,
+            e = launch(phase_ts ? gvr_refine_kernel<true> : gvr_refine_kernel<false>, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, scores,
                        row_stride, row_lens, (int)k,
                        (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts, false, ctl);
         if (e == cudaSuccess)
@@ -579,7 +600,7 @@ gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32
     }
     if ((st = set_smem(indexer_guess_kernel, IXG_SMEM_BYTES)) != GVR_OK ||
         (st = set_smem(indexer_filter_kernel, IXF_SMEM_BYTES)) != GVR_OK ||
-        (st = set_smem(gvr_refine_kernel, RF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(gvr_refine_kernel<false>, RF_SMEM_BYTES)) != GVR_OK ||
         (st = set_smem(indexer_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK)
         return st;
     // the candidate lists of the batch filter path, one filter CTA per SM
@@ -643,7 +664,7 @@ gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32
     if (e == cudaSuccess)
         e = launch(indexer_filter_kernel, cl.G, IX_NT, IXF_SMEM_BYTES, ia, sc, row_lens, (int)k, gpc, cl, bq);
     if (e == cudaSuccess)
-        e = launch(gvr_refine_kernel, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, sc, n_max,
+        e = launch(gvr_refine_kernel<false>, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, sc, n_max,
                    row_lens, (int)k, (int)num_rows, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, gpc, cl, bq,
                    (long long*)nullptr, true, ctl);
     if (e == cudaSuccess)

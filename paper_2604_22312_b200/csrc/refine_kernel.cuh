@@ -22,62 +22,261 @@
 
 namespace gvr {
 
-constexpr int RF_NT = 256;
+#ifndef GVR_RF_NT
+#define GVR_RF_NT 512
+#endif
+#ifndef GVR_RF_HOLD
+#define GVR_RF_HOLD 8
+#endif
+#ifndef GVR_RF_CPS
+#define GVR_RF_CPS 2
+#endif
+#ifndef GVR_RF_NBINS
+#define GVR_RF_NBINS 2048
+#endif
+constexpr int RF_NT = GVR_RF_NT;
+constexpr int RF_NBINS = GVR_RF_NBINS;  // Phase-4 bins of the refine (finer than NBINS: shorter in-bin ranking)
 constexpr int RF_CSORT = 2560;     // entries up to the K-th bin sorted in shared memory
 constexpr int RF_MAXLIST = 1 << 22;  // longest list refined here
 constexpr int RF_BIN_FAST = 16;    // largest bin ranked without narrowing first
 using RefineGroup = Group<RF_NT, 1>;
 constexpr int RF_OFF_HIST = 0;                       // int32 bin counts
-constexpr int RF_OFF_CUR = RF_OFF_HIST + NBINS * 4;  // int32 bin cursors
-constexpr int RF_OFF_CS = RF_OFF_CUR + NBINS * 4;
-constexpr int RF_OFF_ROW = RF_OFF_CS + RF_CSORT * 8;
+constexpr int RF_OFF_CUR = RF_OFF_HIST + RF_NBINS * 4;  // int32 bin cursors
+constexpr int RF_OFF_CS = RF_OFF_CUR + RF_NBINS * 4;
+constexpr int RF_PAD = 16;    // zero composites past the sorted prefix (fixed rank window)
+constexpr int RF_OFF_ROW = RF_OFF_CS + (RF_CSORT + RF_PAD) * 8;
 constexpr int RF_OFF_SCR = RF_OFF_ROW + 16;
 constexpr int RF_SMEM_BYTES = RF_OFF_SCR + GROUP_SCRATCH_BYTES;
-constexpr int RF_CTAS_PER_SM = 4;  // one wave for a decode batch: the per-row work is latency bound
+constexpr int RF_CTAS_PER_SM = GVR_RF_CPS;  // the list is held in registers (RF_HOLD slots per thread)
 static_assert(RF_CTAS_PER_SM * (RF_SMEM_BYTES + 1024) <= 233472, "refine CTAs per SM");
 
 
-// Visit the row's list in batches of UNR entries per thread, segment by segment (segment s:
-// n[s] entries from region position gs[s]; a row with len <= k is one segment read from
-// the row itself, rowx).  fn(kv, aux, valid) gets the keys, a validity mask and per entry
-// either its region position (or row position) or, WITH_IDX, its row index (the entry's
-// second word, loaded with the key).
-template <int UNR, bool WITH_IDX = false, class Fn>
-__device__ __forceinline__ void for_list(const RefineGroup& c, const CandLists& cl, const float* rowx,
-                                         const int (&gs)[F_SEGS], const int (&n)[F_SEGS], Fn&& fn)
-{
-    const uint32_t* rk = reinterpret_cast<const uint32_t*>(cl.region);
-#pragma unroll
-    for (int s = 0; s < F_SEGS; ++s) {
-        const int base = gs[s], ns = n[s];
-        for (int j0 = c.tid; j0 < ns; j0 += UNR * RF_NT) {
-            uint32_t kv[UNR];
-            int aux[UNR];
-            uint32_t valid = 0u;
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int j = j0 + u * RF_NT;
-                const int pos = base + j;
-                kv[u] = 0u;
-                aux[u] = pos;
-                if (j < ns) {
-                    if (rowx) {
-                        kv[u] = f2key(__ldg(rowx + pos));
-                    } else if (WITH_IDX) {
-                        const uint2 e = __ldcg(cl.region + pos);
-                        kv[u] = e.x;
-                        aux[u] = (int)e.y;
-                    } else {
-                        kv[u] = __ldcg(rk + 2 * (size_t)pos);
-                    }
-                    valid |= 1u << u;
-                }
-            }
-            fn(kv, aux, valid);
+// ---- Phase 4 over a row's list, instruction-lean (r2): the list is loaded once into
+// registers (RF_HOLD slots per thread: flat slot j = tid + RF_NT u of the row's
+// concatenated segments), every histogram level and the scatter run from the registers,
+// and the shared-memory atomics are predicated instead of branched around.
+constexpr int RF_HOLD = GVR_RF_HOLD;  // list entries per thread held in registers (RF_HOLD * RF_NT per row)
+
+// A row's list: its <= F_SEGS segments of the filter regions as one flat sequence.
+// tab (shared memory, written by the records step): {p_s, o_s} per segment s — the
+// first flat slot of segment s (a trailing empty segment starts at `total`) and region
+// position minus flat slot.  map() copies it into registers for a batch of loads.
+struct ListSrc {
+    const uint2* region;
+    const int32_t* tab;
+    struct Map {
+        const uint2* region;
+        int o0, p1, o1, p2, o2, p3, o3;
+        __device__ __forceinline__ uint2 load(int j) const
+        {
+            int pos = j + o0;
+            pos = j >= p1 ? j + o1 : pos;
+            pos = j >= p2 ? j + o2 : pos;
+            pos = j >= p3 ? j + o3 : pos;
+            return __ldcg(region + pos);
         }
+    };
+    __device__ __forceinline__ Map map() const
+    {
+        static_assert(F_SEGS == 4, "four list segments");
+        const int4 t0 = reinterpret_cast<const int4*>(tab)[0], t1 = reinterpret_cast<const int4*>(tab)[1];
+        return Map{region, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
     }
+};
+// A row with len <= k: the row itself (key, position).
+struct RowSrc {
+    const float* x;
+    struct Map {
+        const float* x;
+        __device__ __forceinline__ uint2 load(int j) const { return make_uint2(f2key(__ldg(x + j)), (uint32_t)j); }
+    };
+    __device__ __forceinline__ Map map() const { return Map{x}; }
+};
+
+// floor(2^32 RF_NBINS / range), saturated: d -> floor(d scale / 2^32) maps [0, range) onto the bins
+__device__ __forceinline__ uint32_t rf_scale(uint64_t range)
+{
+    const unsigned long long q = (((unsigned long long)RF_NBINS) << 32) / range;
+    return q > 0xffffffffull ? 0xffffffffu : (uint32_t)q;
+}
+// Descending linear bin of key >= lo over [lo, lo + range): bin 0 holds the largest keys.
+__device__ __forceinline__ int rbin(uint32_t key, uint32_t lo, uint32_t scale)
+{
+    return (RF_NBINS - 1) - min((int)__umulhi(key - lo, scale), RF_NBINS - 1);
+}
+__device__ __forceinline__ void red_inc_if(int32_t* p, bool pred)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], 1;\n\t}" ::"r"(smem_u32(p)),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+// if pred: cs[cur[b]++] = (key << 32) | ~idx
+__device__ __forceinline__ void scatter_if(int32_t* curb, unsigned long long* cs, uint32_t key, uint32_t idx, bool pred)
+{
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 s, a;\n\tmov.u32 s, 0;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+        "@q atom.shared.add.u32 s, [%0], 1;\n\tshl.b32 a, s, 3;\n\tadd.u32 a, a, %1;\n\t"
+        "@q st.shared.v2.u32 [a], {%3, %4};\n\t}" ::"r"(smem_u32(curb)),
+        "r"(smem_u32(cs)), "r"((uint32_t)pred), "r"(~idx), "r"(key)
+        : "memory");
 }
 
+// Phase 4 fused with the ordered output (R28, R32) over
+// `total` entries of src, keys >= lo selected: 2048-bin linear histogram over
+// [lo, kmax] (bin 0 = highest), the bin holding position take-1 from the bin scan,
+// narrowing (<= 3 levels) when the bins up to it are crowded, then the entries up to
+// that bin counting-sorted into cs as 64-bit composites and ranked inside their bins;
+// position j < take goes to o[j] / ov[j].  Returns false (group-uniform) when the row
+// cannot be finished here.  ftc = f(lo) of the first level; levels = histogram passes.
+template <class Src>
+__device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, int total, uint32_t lo, uint32_t kmax,
+                                              int take, int32_t* hist, int32_t* cur, unsigned long long* cs,
+                                              int32_t* o, float* ov, int& ftc, int& levels, int& next_slot,
+                                              int32_t* qhead, bool timing, long long (&ts)[TS_N])
+{
+    constexpr int BPT = RF_NBINS / RF_NT;
+    // held slots of this thread: u < nv
+    const int nv = total > c.tid ? min(RF_HOLD, (total - c.tid + RF_NT - 1) / RF_NT) : 0;
+    uint2 e[RF_HOLD];
+    {
+        const auto m = src.map();
+#pragma unroll
+        for (int u = 0; u < RF_HOLD; ++u) e[u] = u < nv ? m.load(c.tid + u * RF_NT) : make_uint2(0u, 0u);
+    }
+    uint32_t scale = 0u, off0 = 0u;
+    const int b0 = c.tid * BPT;
+    int h[BPT];
+    int bk = -1, nsel = 0;
+    bool ok = false;
+    for (int lvl = 0; lvl < 3; ++lvl) {
+        levels = lvl + 1;
+#pragma unroll
+        for (int i = 0; i < BPT / 4; ++i) reinterpret_cast<int4*>(hist + b0)[i] = make_int4(0, 0, 0, 0);
+        if (c.tid == 0) {
+            c.misc[12] = -1;  // K-th bin: set below by the thread that holds it
+            c.misc[14] = (int)rf_scale((uint64_t)kmax - lo + 1ull);  // one 64-bit division per level
+        }
+        c.sync();
+        scale = (uint32_t)c.misc[14];
+        uint32_t f = 0;
+#pragma unroll
+        for (int u = 0; u < RF_HOLD; ++u) {
+            if (u * RF_NT >= total) break;  // group-uniform
+            const bool in = u < nv && e[u].x >= lo;
+            red_inc_if(hist + rbin(e[u].x, lo, scale), in);
+            f += in ? 1u : 0u;
+        }
+        for (int j = c.tid + RF_HOLD * RF_NT; j < total; j += RF_NT) {  // entries past the held slots
+            const uint32_t kv = src.map().load(j).x;                       // (rare: lists > RF_HOLD RF_NT)
+            red_inc_if(hist + rbin(kv, lo, scale), kv >= lo);
+            f += kv >= lo ? 1u : 0u;
+        }
+        f = group_red1<R_ADD>(c, f);  // its barrier also completes the histogram
+        if (lvl == 0) {
+            ftc = (int)f;
+            if (timing) ts[TS_STREAM] = clock64();
+        }
+        uint32_t loc = 0;
+#pragma unroll
+        for (int i = 0; i < BPT / 4; ++i) {
+            const int4 hv = reinterpret_cast<const int4*>(hist + b0)[i];
+            h[4 * i] = hv.x, h[4 * i + 1] = hv.y, h[4 * i + 2] = hv.z, h[4 * i + 3] = hv.w;
+        }
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) loc += (uint32_t)h[i];
+        uint32_t tot;
+        off0 = group_excl_scan(c, loc, tot);
+        {
+            uint32_t off = off0;
+#pragma unroll
+            for (int i = 0; i < BPT; ++i) {
+                if ((uint32_t)(take - 1) >= off && (uint32_t)(take - 1) < off + (uint32_t)h[i]) {
+                    c.misc[12] = b0 + i;
+                    c.misc[13] = (int)(off + (uint32_t)h[i]);
+                }
+                off += (uint32_t)h[i];
+            }
+        }
+        c.sync();
+        bk = ftc >= take ? c.misc[12] : -1;
+        nsel = c.misc[13];
+        uint32_t mx = 0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i)
+            if (b0 + i <= bk) mx = max(mx, (uint32_t)h[i]);
+        mx = group_red1<R_MAX>(c, mx);
+        ok = bk >= 0 && nsel <= RF_CSORT && mx <= (uint32_t)CSORT_BIN_MAX;  // group-uniform
+        // narrow also when the ranking would loop over bins of more than RF_BIN_FAST
+        if (bk < 0 || lvl == 2 || (ok && mx <= (uint32_t)RF_BIN_FAST)) break;
+        // lower edge of bin bk: the smallest d with floor(d scale / 2^32) = RF_NBINS - 1 - bk
+        const uint64_t L = (uint64_t)(RF_NBINS - 1 - bk);
+        const uint64_t dmin = ((L << 32) + scale - 1ull) / scale;
+        if (dmin == 0ull) break;  // the K-th bin is the lowest: narrowing cannot help
+        lo += (uint32_t)dmin;
+    }
+    if (timing) ts[TS_PHASE23] = clock64();
+    if (!ok) return false;
+    {
+        // bin starts; they become the bin ends after the scatter
+        int st[BPT];
+        int off = (int)off0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            st[i] = off;
+            off += h[i];
+        }
+#pragma unroll
+        for (int i = 0; i < BPT / 4; ++i)
+            reinterpret_cast<int4*>(cur + b0)[i] = make_int4(st[4 * i], st[4 * i + 1], st[4 * i + 2], st[4 * i + 3]);
+    }
+    if (c.tid < RF_PAD) cs[nsel + c.tid] = 0ull;  // the rank window may run past the last bin
+    c.sync();
+    // ---- counting sort of the bins up to the K-th bin (composites)
+#pragma unroll
+    for (int u = 0; u < RF_HOLD; ++u) {
+        if (u * RF_NT >= total) break;
+        const int b = rbin(e[u].x, lo, scale);
+        scatter_if(cur + b, cs, e[u].x, e[u].y, u < nv && e[u].x >= lo && b <= bk);
+    }
+    for (int j = c.tid + RF_HOLD * RF_NT; j < total; j += RF_NT) {
+        const uint2 x = src.map().load(j);
+        const int b = rbin(x.x, lo, scale);
+        scatter_if(cur + b, cs, x.x, x.y, x.x >= lo && b <= bk);
+    }
+    c.sync();
+    if (timing) ts[TS_PHASE4] = clock64();
+    if (c.tid == 0 && qhead) next_slot = atomicAdd(qhead, 1);
+    // ---- rank inside the bin; positions < take are the ordered output.  Bins are
+    // contiguous in cs in descending key order, so counting the larger composites over a
+    // fixed window from the bin start (later bins and the zero padding are all smaller)
+    // ranks every entry of a bin of at most RF_PAD entries without a per-compare bound.
+    for (int j = c.tid; j < nsel; j += RF_NT) {
+        const unsigned long long v = cs[j];
+        const int b = rbin(comp_key(v), lo, scale);
+        const int cnt = hist[b];
+        const int st = cur[b] - cnt;
+        const int wmax = (int)__reduce_max_sync(__activemask(), (uint32_t)cnt);
+        int rank = 0;
+        if (wmax <= RF_PAD) {
+#pragma unroll
+            for (int t = 0; t < RF_PAD; t += 4) {
+                if (t >= wmax) break;
+                rank += (cs[st + t] > v ? 1 : 0) + (cs[st + t + 1] > v ? 1 : 0) + (cs[st + t + 2] > v ? 1 : 0) +
+                        (cs[st + t + 3] > v ? 1 : 0);
+            }
+        } else {
+            for (int t = 0; t < cnt; ++t) rank += cs[st + t] > v ? 1 : 0;
+        }
+        const int pos = st + rank;
+        if (pos < take) {
+            o[pos] = comp_idx(v);
+            if (ov) ov[pos] = key2f(comp_key(v));
+        }
+    }
+    return true;
+}
+
+template <bool TIMING>
 __global__ void __launch_bounds__(RF_NT, RF_CTAS_PER_SM)
 gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   int num_rows, int32_t* out, float* out_val, gvr_row_stats* stats, const GuessOut* gp, CandLists cl,
@@ -98,8 +297,6 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     RefineGroup c;
     c.init(threadIdx.x, smem + RF_OFF_SCR);
     const int K = k;
-    constexpr int BPT = NBINS / RF_NT;
-    constexpr int UNR = 8;
     // thread 0 claims the next queue slot during the current row's last step (ranking),
     // so the claim's round trip is off the critical path without hoarding rows early
     int next_slot = -1;
@@ -119,7 +316,8 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         c.sync();
         const int r = *sh_row;
         if (r < 0) break;
-        long long tsr[TS_N] = {phase_ts ? clock64() : 0ll, 0, 0, 0, 0, 0, phase_ts ? global_ns() : 0ll, 0, 0};
+        const bool timing = TIMING && phase_ts != nullptr;  // (the TIMING=false instance has no stamps)
+        long long tsr[TS_N] = {timing ? clock64() : 0ll, 0, 0, 0, 0, 0, timing ? global_ns() : 0ll, 0, 0};
         // the segment records, the row length and T_c are loaded together (the records of
         // slots past the row's segment count are stale and ignored)
         const int4 erec = c.warp == 0 && c.lane < F_SEGS ? __ldcg(cl.rec + (long long)r * F_SEGS + c.lane)
@@ -148,9 +346,18 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             bad = __any_sync(FULL, bad);
             const int tot = (int)__reduce_add_sync(FULL, (uint32_t)n);
             km = __reduce_max_sync(FULL, km);
+            // the flat-slot table of the list (ListSrc): segment s starts at flat slot
+            // p_s = n_0 + ... + n_{s-1}; its region positions are flat slot + o_s
+            uint32_t ps = n;
+#pragma unroll
+            for (int o = 1; o < F_SEGS; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, ps, o);
+                if (c.lane >= o) ps += y;
+            }
+            ps -= (uint32_t)n;
             if (c.lane < F_SEGS) {
-                c.misc[24 + 2 * c.lane] = gsv;
-                c.misc[25 + 2 * c.lane] = n;
+                c.misc[24 + 2 * c.lane] = (int)ps;
+                c.misc[25 + 2 * c.lane] = gsv - (int)ps;
             }
             if (c.lane == 0) {
                 c.misc[22] = bad ? -1 : tot;
@@ -159,17 +366,9 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             }
         }
         c.sync();
-        int gs[F_SEGS], ns[F_SEGS];
-#pragma unroll
-        for (int s = 0; s < F_SEGS; ++s) gs[s] = ns[s] = 0;
         if (p.ntiles > 0) {
             total = c.misc[22];
             kmax = (uint32_t)c.misc[23];
-#pragma unroll
-            for (int s = 0; s < F_SEGS; ++s) {
-                gs[s] = c.misc[24 + 2 * s];
-                ns[s] = c.misc[25 + 2 * s];
-            }
         }
         bool ok = p.ntiles > 0 && p.n > k && total >= K && total <= RF_MAXLIST && kmax >= Tc;
         // a Phase-2 ties exit collected the keys strictly above the tied key (R37): when
@@ -196,146 +395,27 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             rowx = p.x;
             total = p.n;
             take = p.n;
-            gs[0] = 0;  // one segment: the row itself
-            ns[0] = p.n;
-#pragma unroll
-            for (int s = 1; s < F_SEGS; ++s) ns[s] = 0;
             Tc = mn;
             kmax = mx2;
             ok = p.n > 0;
         }
-        if (phase_ts) tsr[TS_PHASE1] = clock64();
-        int ftc = 0, nsel = 0, levels = 0;
+        if (timing) tsr[TS_PHASE1] = clock64();
+        int ftc = 0, levels = 0;
         if (ok && take > 0) {
-            // ---- Phase 4: histogram of the keys >= lo over [lo, kmax],
-            // the K-th bin from the bin scan.  lo starts at T_c; if the
-            // bins up to the K-th one are too crowded to rank (keys spread over a wide key
-            // range, e.g. both signs, leave the top K in few linear bins), lo is raised to
-            // the K-th bin's lower edge and the histogram redone over the narrower range
-            // (every key >= lo still holds the first `take` positions).
-            uint32_t lo = Tc, scale = 0u, off0 = 0u;
-            const int b0 = c.tid * BPT;
-            int h[BPT];
-            int bk = -1;
-            for (int lvl = 0; lvl < 3; ++lvl) {
-                levels = lvl + 1;
-                reinterpret_cast<int4*>(hist + b0)[0] = make_int4(0, 0, 0, 0);
-                reinterpret_cast<int4*>(hist + b0)[1] = make_int4(0, 0, 0, 0);
-                if (c.tid == 0) c.misc[12] = -1;  // K-th bin: set below by the thread that holds it
-                c.sync();
-                scale = bin_scale((uint64_t)kmax - lo + 1ull);
-                uint32_t f = 0;
-                for_list<16>(c, cl, rowx, gs, ns, [&](const uint32_t (&kv)[16], const int (&)[16], uint32_t valid) {
-#pragma unroll
-                    for (int u = 0; u < 16; ++u)
-                        if ((valid >> u & 1u) && kv[u] >= lo) {
-                            atomicAdd(&hist[(NBINS - 1) - lin_bin(kv[u] - lo, scale)], 1);
-                            ++f;
-                        }
-                });
-                f = group_red1<R_ADD>(c, f);  // its barrier also completes the histogram
-                if (lvl == 0) {
-                    ftc = (int)f;
-                    if (phase_ts) tsr[TS_STREAM] = clock64();
-                }
-                uint32_t loc = 0;
-                {
-                    const int4 h0 = reinterpret_cast<const int4*>(hist + b0)[0];
-                    const int4 h1 = reinterpret_cast<const int4*>(hist + b0)[1];
-                    h[0] = h0.x, h[1] = h0.y, h[2] = h0.z, h[3] = h0.w;
-                    h[4] = h1.x, h[5] = h1.y, h[6] = h1.z, h[7] = h1.w;
-                }
-#pragma unroll
-                for (int i = 0; i < BPT; ++i) loc += (uint32_t)h[i];
-                uint32_t tot;
-                off0 = group_excl_scan(c, loc, tot);
-                {
-                    uint32_t off = off0;
-#pragma unroll
-                    for (int i = 0; i < BPT; ++i) {
-                        if ((uint32_t)(take - 1) >= off && (uint32_t)(take - 1) < off + (uint32_t)h[i]) {
-                            c.misc[12] = b0 + i;
-                            c.misc[13] = (int)(off + (uint32_t)h[i]);
-                        }
-                        off += (uint32_t)h[i];
-                    }
-                }
-                c.sync();
-                bk = ftc >= take ? c.misc[12] : -1;
-                nsel = c.misc[13];
-                uint32_t mx = 0;
-#pragma unroll
-                for (int i = 0; i < BPT; ++i)
-                    if (b0 + i <= bk) mx = max(mx, (uint32_t)h[i]);
-                mx = group_red1<R_MAX>(c, mx);
-                ok = bk >= 0 && nsel <= RF_CSORT && mx <= (uint32_t)CSORT_BIN_MAX;  // group-uniform
-                // narrow also when the ranking would loop over bins of more than RF_BIN_FAST
-                if (bk < 0 || lvl == 2 || (ok && mx <= (uint32_t)RF_BIN_FAST)) break;
-                // lower edge of bin bk: the smallest d with lin_bin(d) = NBINS - 1 - bk
-                const uint64_t L = (uint64_t)(NBINS - 1 - bk);
-                const uint64_t dmin = ((L << 32) + scale - 1ull) / scale;
-                if (dmin == 0ull) break;  // the K-th bin is the lowest: narrowing cannot help
-                lo += (uint32_t)dmin;
+            int32_t* o = out + (int64_t)r * k;
+            float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
+            if (rowx) {
+                ok = refine_phase4(c, RowSrc{rowx}, total, Tc, kmax, take, hist, cur, cs, o, ov, ftc, levels,
+                                   next_slot, bq.qctl + Q_HEAD, timing, tsr);
+            } else {
+                ok = refine_phase4(c, ListSrc{cl.region, c.misc + 24}, total, Tc, kmax, take, hist, cur, cs, o, ov, ftc, levels, next_slot,
+                                   bq.qctl + Q_HEAD, timing, tsr);
             }
-            if (phase_ts) tsr[TS_PHASE23] = clock64();
-            if (ok) {
-                {
-                    // bin starts; they become the bin ends after the scatter
-                    int st[BPT];
-                    int off = (int)off0;
-#pragma unroll
-                    for (int i = 0; i < BPT; ++i) {
-                        st[i] = off;
-                        off += h[i];
-                    }
-                    reinterpret_cast<int4*>(cur + b0)[0] = make_int4(st[0], st[1], st[2], st[3]);
-                    reinterpret_cast<int4*>(cur + b0)[1] = make_int4(st[4], st[5], st[6], st[7]);
+            if (ok && !tie_fill)
+                for (int j = take + c.tid; j < k; j += RF_NT) {  // len < k: -1 padding
+                    o[j] = -1;
+                    if (ov) ov[j] = 0.f;
                 }
-                c.sync();
-                // ---- counting sort of the bins up to the K-th bin (composites)
-                for_list<UNR, true>(c, cl, rowx, gs, ns, [&](const uint32_t (&kv)[UNR], const int (&ix)[UNR], uint32_t valid) {
-#pragma unroll
-                    for (int u = 0; u < UNR; ++u) {
-                        const int b = (valid >> u & 1u) && kv[u] >= lo ? (NBINS - 1) - lin_bin(kv[u] - lo, scale) : NBINS;
-                        if (b <= bk) cs[atomicAdd(&cur[b], 1)] = make_comp(kv[u], ix[u]);
-                    }
-                });
-                c.sync();
-                if (phase_ts) tsr[TS_PHASE4] = clock64();
-                if (c.tid == 0) next_slot = atomicAdd(bq.qctl + Q_HEAD, 1);
-                // ---- rank inside the bin; positions < K are the ordered output
-                int32_t* o = out + (int64_t)r * k;
-                float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
-                for (int j = c.tid; j < nsel; j += RF_NT) {
-                    const unsigned long long v = cs[j];
-                    const int b = (NBINS - 1) - lin_bin(comp_key(v) - lo, scale);
-                    const int cnt = hist[b];
-                    const int st = cur[b] - cnt;
-                    const int wmax = (int)__reduce_max_sync(__activemask(), (uint32_t)cnt);
-                    int rank = 0;
-                    if (wmax <= 4) {
-#pragma unroll
-                        for (int t = 0; t < 4; ++t)
-                            if (t < cnt) rank += cs[st + t] > v;
-                    } else if (wmax <= 8) {
-#pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            if (t < cnt) rank += cs[st + t] > v;
-                    } else {
-                        for (int i2 = st; i2 < st + cnt; ++i2) rank += cs[i2] > v;
-                    }
-                    const int pos = st + rank;
-                    if (pos < take) {
-                        o[pos] = comp_idx(v);
-                        if (ov) ov[pos] = key2f(comp_key(v));
-                    }
-                }
-                if (!tie_fill)
-                    for (int j = take + c.tid; j < k; j += RF_NT) {  // len < k: -1 padding
-                        o[j] = -1;
-                        if (ov) ov[j] = 0.f;
-                    }
-            }
         }
         if (ok && tie_fill) {
             // positions [take, K): the first K - take elements of the row equal to the tied
@@ -396,7 +476,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
                 s.reserved = 0;
                 stats[r] = s;
             }
-            if (phase_ts && ok) {
+            if (timing && ok) {
                 tsr[TS_END] = clock64();
                 tsr[TS_GEND] = global_ns();
                 tsr[TS_SMID] = sm_id();
