@@ -237,14 +237,17 @@ const char* gvr_last_cuda_error(void);
 /* Library/ABI version: major*10000 + minor*100 + patch. */
 int32_t gvr_version(void);
 
-/* Filter-kernel timeline (diagnostics): enable = 1 starts recording, for
- * every gvr_filter_kernel CTA b < 4096 of the following calls, globaltimer (ns) at entry,
- * after its wait for Phases 1-2, and at exit, plus its SM id; enable = 0 synchronizes
- * the device, copies min(max_ctas, 4096) records of 4 int64 each into host_out (caller-
+/* CTA timeline of the batch filter path (diagnostics).  kernel = 0: the
+ * gvr_filter_kernel CTAs b < 4096 — globaltimer (ns) at entry, after the wait for Phases
+ * 1-2, at exit, and the SM id; kernel = 1: the gvr_guess_kernel CTAs (one per row, rows
+ * < 4096) — globaltimer at entry, at exit, when its loads have arrived and after Phase 1.  enable = 1 starts recording
+ * (both kernels) for the following calls; enable = 0 synchronizes the device, copies
+ * min(max_ctas, 4096) records of 4 int64 each of the chosen kernel into host_out (caller-
  * owned, 4 * max_ctas int64), stores the count in *n_out (may be NULL) and stops recording.
  * Records of CTAs that did not run since enabling are stale.  GVR_ERR_INVALID_ARGUMENT for
- * host_out == NULL or max_ctas < 0 when enable == 0; GVR_ERR_CUDA on a CUDA failure. */
-gvr_status gvr_filter_cta_times(int32_t enable, int64_t* host_out, int32_t max_ctas, int32_t* n_out);
+ * a kernel other than 0/1, or host_out == NULL or max_ctas < 0 when enable == 0;
+ * GVR_ERR_CUDA on a CUDA failure. */
+gvr_status gvr_cta_timeline(int32_t kernel, int32_t enable, int64_t* host_out, int32_t max_ctas, int32_t* n_out);
 
 /* Launch geometry of the two kernels on the current device (diagnostics): resident CTAs
  * per SM, threads per CTA and dynamic shared memory per CTA.  Any pointer may be NULL.

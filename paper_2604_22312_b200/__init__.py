@@ -77,9 +77,9 @@ def _load():
     lib.gvr_last_cuda_error.restype = ctypes.c_char_p
     lib.gvr_version.argtypes = []
     lib.gvr_version.restype = ctypes.c_int32
-    lib.gvr_filter_cta_times.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32,
-                                         ctypes.POINTER(ctypes.c_int32)]
-    lib.gvr_filter_cta_times.restype = ctypes.c_int
+    lib.gvr_cta_timeline.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32,
+                                     ctypes.POINTER(ctypes.c_int32)]
+    lib.gvr_cta_timeline.restype = ctypes.c_int
     lib.gvr_kernel_info.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 6
     lib.gvr_kernel_info.restype = ctypes.c_int
     _lib = lib
@@ -91,17 +91,19 @@ def library():
     return _load()
 
 
-def filter_cta_times(enable: bool, max_ctas: int = 4096):
-    """gvr_filter_cta_times: enable=True starts recording the filter kernel's per-CTA
-    timeline; enable=False stops and returns an int64 array [n, 4] (entry ns, after the
-    Phase-1/2 wait ns, exit ns, SM id)."""
+def cta_timeline(enable: bool, kernel: str = "filter", max_ctas: int = 4096):
+    """gvr_cta_timeline: enable=True starts recording the filter path's CTA timeline;
+    enable=False stops and returns an int64 array [n, 4] for kernel "filter" (entry ns,
+    after the Phase-1/2 wait ns, exit ns, SM id) or "guess" (entry ns, exit ns, loads arrived ns, Phase 1 done ns).
+    Call enable=False once per kernel wanted (the first call stops recording)."""
     import numpy as np
+    kid = {"filter": 0, "guess": 1}[kernel]
     if enable:
-        _check(_load().gvr_filter_cta_times(1, None, 0, None))
+        _check(_load().gvr_cta_timeline(kid, 1, None, 0, None))
         return None
     out = np.zeros((max_ctas, 4), dtype=np.int64)
     n = ctypes.c_int32(0)
-    _check(_load().gvr_filter_cta_times(0, out.ctypes.data, max_ctas, ctypes.byref(n)))
+    _check(_load().gvr_cta_timeline(kid, 0, out.ctypes.data, max_ctas, ctypes.byref(n)))
     return out[:n.value]
 
 

@@ -108,12 +108,6 @@ __device__ __forceinline__ void issue_pair(const Ring& ring, const RoundIter& it
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ring.full(s0 + 1)) : "memory");
 }
 
-// Diagnostics (gvr_filter_cta_times): per filter CTA, globaltimer at entry, after the
-// Phase-1/2 wait and at exit, recorded while g_fts_on is set.
-constexpr int FTS_MAX = 4096;
-__device__ int g_fts_on;
-__device__ long long g_fts[FTS_MAX][4];
-
 __global__ void __launch_bounds__(F_NT, F_CTAS_PER_SM)
 gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   const GuessOut* __restrict__ gp, CandLists cl, BatchQueue bq)

@@ -85,6 +85,14 @@ __device__ __forceinline__ long long sm_id()
     return (long long)s;
 }
 
+// Diagnostics (gvr_cta_timeline), recorded while g_fts_on is set: per gvr_filter_kernel CTA
+// b < FTS_MAX globaltimer at entry, after the Phase-1/2 wait and at exit, and its SM id;
+// per gvr_guess_kernel CTA (row) globaltimer at entry and exit and its SM id.
+constexpr int FTS_MAX = 4096;
+__device__ int g_fts_on;
+__device__ long long g_fts[FTS_MAX][4];
+__device__ long long g_gts[FTS_MAX][4];
+
 // What Phases 1-2 (phase12) hand to the streaming step, per row (32 bytes).
 struct GuessOut {
     uint32_t Tc;     // collect threshold key (Phase 2 result)
@@ -622,8 +630,23 @@ __device__ __forceinline__ float group_fsum1(G& c, float a)
 }
 
 // Phase-2 constants (R34-R36).
-constexpr int P2_CHUNK = 16;                 // floats per sample chunk (one 64-byte read)
+constexpr int P2_CHUNK = 16;                 // sample floats per thread (one 64-byte read)
 constexpr int P2_S = 256 * P2_CHUNK;         // sample values: one chunk per thread
+#ifndef GVR_P2_RUN
+#define GVR_P2_RUN 64
+#endif
+constexpr int P2_RUN = GVR_P2_RUN;           // floats per contiguous sample run (P2_RUN / 16 threads)
+constexpr int P2_TPR = P2_RUN / P2_CHUNK;    // threads per run
+constexpr int P2_NRUN = 256 / P2_TPR;        // runs per row sample
+static_assert(P2_RUN % P2_CHUNK == 0 && 256 % P2_TPR == 0, "sample runs");
+// Offset (from the 16-byte aligned body start) of thread t's 16 sample floats: run
+// g = t / P2_TPR starts at P2_RUN floor(g nrun / P2_NRUN), nrun = floor(body / P2_RUN),
+// and thread t reads its 16 floats at 16 (t % P2_TPR) inside it (R34).
+__host__ __device__ __forceinline__ int sample_off(int t, int body)
+{
+    const int nrun = body / P2_RUN;
+    return P2_RUN * (int)(((int64_t)(t / P2_TPR) * nrun) / P2_NRUN) + P2_CHUNK * (t % P2_TPR);
+}
 constexpr int P2_MAX_ITERS = 12;             // probes before the Phase-2 fallback (R12)
 constexpr float P2_Z_DEFAULT = 4.5f;
 
@@ -634,8 +657,8 @@ constexpr float P2_Z_DEFAULT = 4.5f;
 //     i = t + 256 j (thread t): m_i = 8 gs floor(i / 8) + i % 8 < k (R29; load_guess_idx)
 //     -> pmin / pmax (keys), pmean = sum / count (Eq. 4).
 //     No valid guess -> the statistics of the row sample.
-//   Sample: chunk t (16 contiguous floats of the 16-byte aligned body, chunk start
-//     16 * floor(t * nch / 256) of nch = body / 16 chunks) in registers, as keys.
+//   Sample: thread t's 16 contiguous floats of the 16-byte aligned body at sample_off(t):
+//     64 runs of 64 floats spread over the row (R34), in registers, as keys.
 //   Phase 2: window [L, H] in sample hits, L = ceil(mu + z sqrt(mu)) with mu = k S / n
 //     the expected hits at the K-th value, H = L + ceil(L / 2), target (L + H) / 2;
 //     anchors exact for the sample: (min key, S), (max key + 1, 0) (R8).  Probe T0 =
@@ -687,10 +710,13 @@ __device__ __forceinline__ void load_guess_idx(const G& c, const int32_t* pr, in
     static_assert(G::N == 256, "eight guess slots per thread");
     const int gs = prm.guess_stride;
 #pragma unroll
+    for (int j = 0; j < GUESS_PER_THREAD; ++j) gi[j] = -1;
+#pragma unroll
     for (int j = 0; j < GUESS_PER_THREAD; ++j) {
+        if (j * G::N * gs >= k) break;  // group-uniform: slot j's smallest rank is 256 gs j
         const int i = c.tid + j * G::N;
         const int m = 8 * gs * (i >> 3) + (i & 7);
-        gi[j] = (pr && m < k) ? __ldg(pr + m) : -1;
+        if (pr && m < k) gi[j] = __ldg(pr + m);
     }
 }
 
@@ -700,7 +726,7 @@ __device__ __forceinline__ void load_guess_idx(const G& c, const int32_t* pr, in
 template <class G>
 __device__ __forceinline__ GuessOut phase12_core(G& c, int n, const float (&gv)[GUESS_PER_THREAD], uint32_t valid,
                                                  const float (&sv)[P2_CHUNK], int k, const GvrParams& prm,
-                                                 int32_t* sh256)
+                                                 int32_t* sh256, long long* ts = nullptr)
 {
     constexpr int GPT = GUESS_PER_THREAD;
     GuessOut g;
@@ -726,6 +752,7 @@ __device__ __forceinline__ GuessOut phase12_core(G& c, int n, const float (&gv)[
         sum = __fadd_rn(sum, gv[j]);  // invalid slots add +0
     }
     group_red4<R_MIN, R_MAX, R_ADD, R_MAX>(c, kmn, kmx, cnt, smax);
+    if (ts && c.tid == 0) ts[2] = global_ns();  // (diagnostics) every load has arrived
     smin = group_red1<R_MIN>(c, smin);
     bool complete = cnt == (uint32_t)k && prm.guess_stride == 1;
     if (cnt == 0) {  // no valid guess: statistics of the row sample (R7)
@@ -739,6 +766,7 @@ __device__ __forceinline__ GuessOut phase12_core(G& c, int n, const float (&gv)[
     }
     sum = group_fsum1(c, sum);
     const float pmean = __fdiv_rn(sum, (float)cnt);
+    if (ts && c.tid == 0) ts[3] = global_ns();  // (diagnostics) Phase 1 done
     // ---- Phase 2 over the sample (Eq. 6)
     const float mu = __fdiv_rn((float)(k * P2_S), (float)n);
     const int L = min(max((int)ceilf(__fadd_rn(mu, __fmul_rn(prm.window_z, __fsqrt_rn(mu)))), 1), P2_S);
@@ -827,7 +855,7 @@ __device__ __forceinline__ GuessOut phase12_core(G& c, int n, const float (&gv)[
 
 template <class G>
 __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_t (&gi)[GUESS_PER_THREAD], int k,
-                                            const GvrParams& prm, int32_t* sh256)
+                                            const GvrParams& prm, int32_t* sh256, long long* ts = nullptr)
 {
     static_assert(G::N == 256, "one sample chunk per thread");
     constexpr int GPT = GUESS_PER_THREAD;  // 8 guessed positions per thread
@@ -845,9 +873,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
         return g;
     }
     // ---- loads: the sample chunk, then the guessed values
-    const int nch = p.nfl / P2_CHUNK;  // >= 376 for n > GVR_CAP
-    const float4* sp4 =
-        reinterpret_cast<const float4*>(p.x + p.head + P2_CHUNK * (int)(((int64_t)c.tid * nch) >> 8));
+    const float4* sp4 = reinterpret_cast<const float4*>(p.x + p.head + sample_off(c.tid, p.nfl));
     float sv[P2_CHUNK];
 #pragma unroll
     for (int q = 0; q < P2_CHUNK / 4; ++q) {
@@ -867,7 +893,7 @@ __device__ __forceinline__ GuessOut phase12(G& c, const RowPlan& p, const int32_
             valid |= 1u << j;
         }
     }
-    return phase12_core(c, p.n, gv, valid, sv, k, prm, sh256);
+    return phase12_core(c, p.n, gv, valid, sv, k, prm, sh256, ts);
 }
 
 
@@ -897,6 +923,8 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     GuessGroup c;
     c.init(threadIdx.x, scratch);
     const int r = blockIdx.x;
+    const bool gts = c.tid == 0 && r < FTS_MAX && *(volatile int*)&g_fts_on;
+    if (gts) g_gts[r][0] = global_ns();
     int32_t gi[GUESS_PER_THREAD];  // issued first: the guess indices do not depend on the row length
     load_guess_idx(c, prev ? prev + (int64_t)r * k : nullptr, k, prm, gi);
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
@@ -908,10 +936,11 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
         return;
     }
     __shared__ int32_t sh[256];
-    GuessOut g = phase12(c, p, gi, k, prm, sh);
+    GuessOut g = phase12(c, p, gi, k, prm, sh, gts ? g_gts[r] : nullptr);
     // filter path, a ties exit: collect the keys strictly above the tie; when they are
     // fewer than K the refine kernel fills the rest with the tie's lowest indices (R37)
     if (bq.queue && g.exit == GVR_P2_TIES && g.tie < 0xffffffffu) g.Tc = g.tie + 1u;
+    if (gts) g_gts[r][1] = global_ns();
     if (c.tid == 0) {
         gp[r] = g;
         if (!bq.queue) {

@@ -223,14 +223,16 @@ const char* gvr_status_string(gvr_status s)
 
 int32_t gvr_version(void) { return kVersion; }
 
-gvr_status gvr_filter_cta_times(int32_t enable, int64_t* host_out, int32_t max_ctas, int32_t* n_out)
+gvr_status gvr_cta_timeline(int32_t kernel, int32_t enable, int64_t* host_out, int32_t max_ctas, int32_t* n_out)
 {
+    if (kernel != 0 && kernel != 1) return GVR_ERR_INVALID_ARGUMENT;
     const int on = enable ? 1 : 0;
     if (!enable) {
         if (!host_out || max_ctas < 0) return GVR_ERR_INVALID_ARGUMENT;
         const int n = min((int)max_ctas, FTS_MAX);
         if (cudaDeviceSynchronize() != cudaSuccess ||
-            cudaMemcpyFromSymbol(host_out, g_fts, (size_t)n * 4 * sizeof(long long)) != cudaSuccess) {
+            (kernel == 0 ? cudaMemcpyFromSymbol(host_out, g_fts, (size_t)n * 4 * sizeof(long long))
+                         : cudaMemcpyFromSymbol(host_out, g_gts, (size_t)n * 4 * sizeof(long long))) != cudaSuccess) {
             g_last_cuda_error = cudaGetLastError();
             return GVR_ERR_CUDA;
         }

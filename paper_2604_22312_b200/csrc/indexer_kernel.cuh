@@ -240,8 +240,8 @@ __device__ __forceinline__ void score_tiles(const QFrag& f, uint32_t kbuf, const
 
 // ---------------------------------------------------------------------------------
 // Fused Phases 1-2 (gvr_indexer_topk_batched): one CTA per row computes the scores at the
-// guessed positions and at the 4096 row-sample positions (16 consecutive keys at
-// 16 floor(c nch / 256), nch = n / 16, for c < 256 — the score path's sample with head 0)
+// guessed positions and at the 4096 row-sample positions (sample_off: 64 runs of 64
+// consecutive keys spread over the row — the score path's sample with head 0)
 // and runs phase12_core on them.  Rows with no tiles go to the ready queue.
 constexpr int IXG_OFF_Q = 0;
 constexpr int IXG_OFF_K = 16384;                       // 4 tile buffers
@@ -290,7 +290,6 @@ indexer_guess_kernel(IndexerArgs ia, const float* __restrict__ scratch, const in
         __syncthreads();
         QFrag f;
         load_qfrag(f, sbase + IXG_OFF_Q, warp, lane);
-        const int nch = n / P2_CHUNK;
         // guessed slots used: blocks of 8 ranks every 8 gs ranks while the rank is < k
         const int gs = prm.guess_stride;
         const int nslots = min(KMAX, 8 * ((k + 8 * gs - 1) / (8 * gs)));
@@ -299,8 +298,8 @@ indexer_guess_kernel(IndexerArgs ia, const float* __restrict__ scratch, const in
             f, sbase + IXG_OFF_K, W, part, kb, P2_S / IX_TILE + gtiles,
             [&](int u, int i) {
                 if (u < P2_S / IX_TILE) {  // sample tile: chunks 4u .. 4u + 3
-                    const int cidx = 4 * u + (i >> 4);
-                    return P2_CHUNK * (int)(((int64_t)cidx * nch) >> 8) + (i & 15);
+                    const int cidx = 4 * u + (i >> 4);  // the thread whose sample value this is
+                    return sample_off(cidx, n) + (i & 15);
                 }
                 const int slot = (u - P2_S / IX_TILE) * IX_TILE + i;
                 return slot < nslots ? gpos[slot] : -1;

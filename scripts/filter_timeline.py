@@ -1,4 +1,4 @@
-"""Filter-kernel CTA timeline on a bench config (gvr_filter_cta_times): when each
+"""Filter-path CTA timeline on a bench config (gvr_cta_timeline): when each
 persistent filter CTA starts, when its wait for Phases 1-2 ends and when it exits, to see
 whether the spread of exit times comes from late starts or from uneven streaming."""
 import os, sys
@@ -17,18 +17,25 @@ torch.cuda.synchronize()
 for rep in range(2):
     flush.zero_()
     torch.cuda.synchronize()
-    gvr.filter_cta_times(True)
+    gvr.cta_timeline(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     gvr.topk(b["scores"], bench.K, row_lens=b["row_lens"], prev=b["prev"])
     e1.record()
-    t = gvr.filter_cta_times(False)
+    t = gvr.cta_timeline(False, "filter")
+    gt = gvr.cta_timeline(False, "guess")[:b["R"]]
     G = 3 * torch.cuda.get_device_properties(0).multi_processor_count
     t = t[:G]
-    t0 = t[:, 0].min()
+    t0 = min(t[:, 0].min(), gt[:, 0].min())
+    gs_, ge_ = (gt[:, 0] - t0) / 1e3, (gt[:, 1] - t0) / 1e3
     st, wt, en = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
     q = lambda a: " ".join(f"{np.percentile(a, p):.1f}" for p in (0, 10, 50, 90, 100))
-    print(f"call {e0.elapsed_time(e1) * 1e3:.1f} us; filter CTAs {G}; times from the first CTA start (us), p0/10/50/90/100")
+    print(f"call {e0.elapsed_time(e1) * 1e3:.1f} us; filter CTAs {G}; times from the first guess CTA start (us), p0/10/50/90/100")
+    print("  guess start", q(gs_))
+    print("  guess end  ", q(ge_))
+    print("  guess dur  ", q(ge_ - gs_))
+    gl_, gp1_ = (gt[:, 2] - t0) / 1e3, (gt[:, 3] - t0) / 1e3
+    print("  guess loads", q(gl_), " phase1 done", q(gp1_), " phase2 dur", q(ge_ - gp1_))
     print("  start      ", q(st))
     print("  wait end   ", q(wt))
     print("  exit       ", q(en))

@@ -67,15 +67,19 @@ def test_window_cfg2_values():
 
 # --------------------------------------------------------------------------- sample layout
 def test_sample_positions_layout():
-    """256 chunks of 16 contiguous floats, chunk c at head + 16 floor(c nch / 256)."""
+    """64 runs of 64 contiguous floats, run g at head + 64 floor(g nrun / 64); thread c
+    reads the 16 floats at 16 (c % 4) inside run c // 4 (DESIGN.md R34)."""
     n, head = 100_003, 3
     pos = P2.sample_positions(n, head)
     assert pos.size == 4096 and len(np.unique(pos)) == 4096
-    nch = (4 * ((n - head) // 4)) // 16
-    for c in (0, 1, 100, 255):
-        start = head + 16 * ((c * nch) // 256)
-        assert list(pos[16 * c:16 * c + 16]) == list(range(start, start + 16))
+    nrun = (4 * ((n - head) // 4)) // 64
+    for g in (0, 1, 33, 63):
+        start = head + 64 * ((g * nrun) // 64)
+        assert list(pos[64 * g:64 * g + 64]) == list(range(start, start + 64))
     assert pos.max() < n and pos.min() == head
+    # runs are spread over the row: consecutive runs start nrun // 64 runs apart (or one more)
+    gaps = np.diff(pos[::64])
+    assert set(gaps) <= {64 * (nrun // 64), 64 * (nrun // 64 + 1)}
 
 
 # --------------------------------------------------------------------------- Phase 1
