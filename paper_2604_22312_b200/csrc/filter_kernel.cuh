@@ -136,8 +136,11 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             issue_pair(ring, prod, issued);
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // gp (Phase 1) is complete and visible
-    if (fts) g_fts[b][1] = global_ns();
+    // (r2) no wait for the whole Phase-1/2 grid: each row's threshold is taken from its
+    // hand-off word (BatchQueue::tcw) once the guess kernel has published it
+    const bool per_row = bq.tcw != nullptr;
+    if (!per_row) asm volatile("griddepcontrol.wait;" ::: "memory");  // gp is complete and visible
+    const uint32_t gen = per_row ? *bq.gen + 1u : 0u;
     c.sync();
     uint2* reg = cl.region + (long long)b * cl.reg;
     const int regcap = cl.reg;
@@ -149,15 +152,29 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     float Tf = 0.f;
     // T_c of the row after the current one, loaded a whole segment ahead of its use
     const int r_first = it.r;
-    uint32_t tc_next = r_first < cl.V / cl.tpr ? __ldcg(&gp[r_first].Tc) : 0u;
+    const int nrows = (int)(cl.V / cl.tpr);
+    // row r's threshold from a (possibly early) read v of its hand-off word: spin until the
+    // word carries this call's generation (acquire; the guess kernel stores it with release)
+    auto tc_of = [&](int r, unsigned long long v) -> uint32_t {
+        if (!per_row) return __ldcg(&gp[r].Tc);
+        while ((uint32_t)(v >> 32) != gen) {
+            __nanosleep(64);
+            v = ld_acquire_u64(bq.tcw + r);
+        }
+        return (uint32_t)v;
+    };
+    auto tc_peek = [&](int r) -> unsigned long long { return per_row ? ld_relaxed_u64(bq.tcw + r) : 0ull; };
+    unsigned long long tc_next = r_first < nrows ? tc_peek(r_first) : 0ull;
     uint32_t kmax = 0u;  // this thread's largest candidate key in the current segment
     for (int i = 0; it.next(scores, stride, row_lens, k, cl.tpr); ++i) {
         const RowPlan& p = it.p;
         if (it.r != cur_r) {
-            const uint32_t tc = it.r == (cur_r < 0 ? r_first : cur_r + 1) ? tc_next : __ldcg(&gp[it.r].Tc);
+            const bool first = cur_r < 0;
+            const uint32_t tc = tc_of(it.r, it.r == (first ? r_first : cur_r + 1) ? tc_next : tc_peek(it.r));
+            if (fts && first) g_fts[b][1] = global_ns();
             cur_r = it.r;
             Tf = key2f(tc);
-            if (cur_r + 1 < cl.V / cl.tpr) tc_next = __ldcg(&gp[cur_r + 1].Tc);
+            if (cur_r + 1 < nrows) tc_next = tc_peek(cur_r + 1);
         }
         // unaligned head scalars (round holding tile 0) and tail scalars (round holding the
         // last tile), loaded before the wait so their latency hides behind it

@@ -139,7 +139,34 @@ struct BatchQueue {
     int32_t* queue;    // [num_rows]: row + 1 once pushed, reset to 0 when popped
     int32_t* segdone;  // [num_rows]: finished filter segments, reset when popped
     int32_t* fixlist;  // [num_rows]
+    // (r2) per-row threshold hand-off from Phases 1-2 to the filter kernel: tcw[r] =
+    // (generation << 32) | T_c, stored with release once row r's GuessOut is written; the
+    // generation is *gen + 1, *gen counting the lease's completed filter-path calls (the
+    // fixup's last CTA increments it).  The filter waits per row, not for the whole grid.
+    uint32_t* gen;
+    unsigned long long* tcw;  // [num_rows]
 };
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Publish row r's threshold (thread 0, after gp[r] is written).
+__device__ __forceinline__ void publish_tc(const BatchQueue& bq, int r, uint32_t Tc)
+{
+    if (bq.tcw) st_release_u64(bq.tcw + r, ((unsigned long long)(*bq.gen + 1u) << 32) | Tc);
+}
 
 __device__ __forceinline__ int ld_relaxed(const int32_t* p)
 {
@@ -943,6 +970,7 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     if (gts) g_gts[r][1] = global_ns();
     if (c.tid == 0) {
         gp[r] = g;
+        publish_tc(bq, r, g.Tc);  // release: gp[r] is visible to whoever sees this word
         if (!bq.queue) {
             if (g.exit == GVR_P2_TIES || g.exit == GVR_P2_EXHAUSTED)
                 sched.order[atomicAdd(sched.cursors, 1)] = r;
@@ -963,6 +991,7 @@ __device__ __forceinline__ void fixup_done(int32_t* ctl, const BatchQueue& bq, i
         ctl[CTL_RDONE] = 0;
         if (bq.qctl)
             for (int i = 0; i < Q_WORDS; ++i) bq.qctl[i] = 0;
+        if (bq.gen) *bq.gen += 1u;  // this call's thresholds are stale from now on
     }
 }
 

@@ -75,8 +75,9 @@ cudaMemPool_t scratch_pool()
 //  * A failed call leaves the slot marked dirty; the next lease clears its zero region.
 //
 // Layout: a zero region at fixed offsets — ctl[4] | qctl[4] | queue[rows_cap] |
-// segdone[rows_cap] — whose words are zero between calls (each kernel resets what it
-// used), sized by the lease's row capacity so that calls with fewer rows leave the tail
+// segdone[rows_cap] | gen, pad | tcw[rows_cap] (8 B) — whose words are zero between calls
+// (each kernel resets what it used; gen counts completed filter-path calls and tcw[r]
+// carries the generation it was written for, so neither needs a reset), sized by the lease's row capacity so that calls with fewer rows leave the tail
 // untouched; then the per-call arrays (zero_region_bytes(rows_cap) onwards).
 struct ScratchSlot {
     void* ptr = nullptr;
@@ -98,7 +99,7 @@ struct ScratchLease {
     }
 };
 
-size_t zero_region_bytes(int64_t rows_cap) { return (32 + 8 * (size_t)rows_cap + 255) & ~(size_t)255; }
+size_t zero_region_bytes(int64_t rows_cap) { return (40 + 16 * (size_t)rows_cap + 255) & ~(size_t)255; }
 
 std::mutex& scratch_mutex()
 {
@@ -427,6 +428,8 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         bq.queue = bq.qctl + 4;
         bq.segdone = bq.queue + lease.rows_cap;
         bq.fixlist = reinterpret_cast<int32_t*>(per_call + fix_off);
+        bq.gen = reinterpret_cast<uint32_t*>(bq.segdone + lease.rows_cap);
+        bq.tcw = reinterpret_cast<unsigned long long*>(scratch + 40 + 8 * (size_t)lease.rows_cap);
         cl.rec = reinterpret_cast<int4*>(per_call + rec_off);
         cl.region = reinterpret_cast<uint2*>(per_call + region_off);
     }

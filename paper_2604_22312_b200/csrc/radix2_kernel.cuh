@@ -163,6 +163,7 @@ radix_thresh_kernel(const float* __restrict__ scores, int64_t stride, const int3
         g.top = 0xffffffffu;
         g.exit = GVR_P2_ALL;
         gp[r] = g;
+        publish_tc(bq, r, g.Tc);
     }
 }
 
