@@ -120,8 +120,10 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     FilterGroup c;
     c.init(threadIdx.x, smem + F_OFF_SCR);
     const int b = blockIdx.x;
-    const bool fts = c.tid == 0 && b < FTS_MAX && *(volatile int*)&g_fts_on;
-    if (fts) g_fts[b][0] = global_ns();
+    // diagnostics: stamps kept in registers, stored at exit if recording is on (the flag is
+    // read last, off the critical path)
+    const long long ts_entry = global_ns();
+    long long ts_wait = 0;
     const long long vb = cl_begin(cl, b), ve = cl_begin(cl, b + 1);
     RoundIter prod;  // thread 0: two rounds ahead of the consumers
     prod.start(vb, ve, cl.tpr);
@@ -171,7 +173,7 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         if (it.r != cur_r) {
             const bool first = cur_r < 0;
             const uint32_t tc = tc_of(it.r, it.r == (first ? r_first : cur_r + 1) ? tc_next : tc_peek(it.r));
-            if (fts && first) g_fts[b][1] = global_ns();
+            if (first) ts_wait = global_ns();
             cur_r = it.r;
             Tf = key2f(tc);
             if (cur_r + 1 < nrows) tc_next = tc_peek(cur_r + 1);
@@ -263,7 +265,9 @@ gvr_filter_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             c.sync();  // no reservation of the next segment before the cursor was read
         }
     }
-    if (fts) {
+    if (c.tid == 0 && b < FTS_MAX && *(volatile int*)&g_fts_on) {
+        g_fts[b][0] = ts_entry;
+        g_fts[b][1] = ts_wait;
         g_fts[b][2] = global_ns();
         g_fts[b][3] = sm_id();
     }

@@ -950,8 +950,8 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
     GuessGroup c;
     c.init(threadIdx.x, scratch);
     const int r = blockIdx.x;
-    const bool gts = c.tid == 0 && r < FTS_MAX && *(volatile int*)&g_fts_on;
-    if (gts) g_gts[r][0] = global_ns();
+    // diagnostics: stamps kept locally, stored at exit if recording is on (flag read last)
+    long long gts_l[4] = {global_ns(), 0, 0, 0};
     int32_t gi[GUESS_PER_THREAD];  // issued first: the guess indices do not depend on the row length
     load_guess_idx(c, prev ? prev + (int64_t)r * k : nullptr, k, prm, gi);
     const RowPlan p = plan_row(scores, stride, row_lens, r, k);
@@ -963,11 +963,16 @@ gvr_guess_kernel(const float* __restrict__ scores, int64_t stride, const int32_t
         return;
     }
     __shared__ int32_t sh[256];
-    GuessOut g = phase12(c, p, gi, k, prm, sh, gts ? g_gts[r] : nullptr);
+    GuessOut g = phase12(c, p, gi, k, prm, sh, gts_l);
     // filter path, a ties exit: collect the keys strictly above the tie; when they are
     // fewer than K the refine kernel fills the rest with the tie's lowest indices (R37)
     if (bq.queue && g.exit == GVR_P2_TIES && g.tie < 0xffffffffu) g.Tc = g.tie + 1u;
-    if (gts) g_gts[r][1] = global_ns();
+    if (c.tid == 0 && r < FTS_MAX && *(volatile int*)&g_fts_on) {
+        g_gts[r][0] = gts_l[0];
+        g_gts[r][1] = global_ns();
+        g_gts[r][2] = gts_l[2];
+        g_gts[r][3] = gts_l[3];
+    }
     if (c.tid == 0) {
         gp[r] = g;
         publish_tc(bq, r, g.Tc);  // release: gp[r] is visible to whoever sees this word
