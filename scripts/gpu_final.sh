@@ -24,3 +24,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 python scripts/traffic_from_ncu.py gvr_cfg2=$O/prof_gvr_filter_kernel.ncu-rep refine_cfg2=$O/prof_gvr_refine_kernel.ncu-rep guess_cfg2=$O/prof_gvr_guess_kernel.ncu-rep > $O/traffic.log 2>&1; cat $O/traffic.log
 cp profiles/traffic.json $O/traffic.json
 for kn in gvr_filter_kernel gvr_refine_kernel gvr_guess_kernel; do echo "== $kn"; tail -22 $O/summary_$kn.txt; done
+timeout 300 python scripts/filter_timeline.py cfg2 > $O/cta_timeline_cfg2.log 2>&1
+timeout 300 python scripts/filter_timeline.py cfg4 > $O/cta_timeline_cfg4.log 2>&1
+timeout 300 python scripts/refine_timing.py > $O/refine_timing_cfg2.log 2>&1
