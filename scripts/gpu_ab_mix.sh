@@ -9,7 +9,7 @@ for r in $(seq ${ROUNDS:-2}); do
     l=${a%%:*}; e=${a#*:}
     cp ab/$l $LIB
     for c in ${CFGS:-cfg2}; do
-      ms=$(env X=1 $e python bench.py --config $c --no-e2e --no-cpu 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['kernel_us_per_launch'])")
+      ms=$(env X=1 $e python bench.py --config $c --no-e2e --no-cpu 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['kernel_us_per_launch'], {k: round(v, 2) for k, v in (d.get('passes_per_row') or {}).items() if k in ('secant_mean', 'cand_mean')})")
       echo "round $r $a $c $ms"
     done
   done

@@ -618,6 +618,52 @@ def test_filter_path_alternating_batch_sizes_and_paths(gvr):
         _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens)
 
 
+def test_threshold_handoff_never_reads_a_stale_generation(gvr):
+    """The filter kernel takes each row's T_c from a generation-tagged word (BatchQueue::tcw)
+    instead of waiting for the guess grid.  Rows of a shrinking then growing batch on one
+    stream reuse words written by earlier calls with other thresholds: every call must be
+    exact (a stale word would hand a row another call's T_c — too high drops rows of the
+    Top-K from the list, too low overflows it)."""
+    import torch
+    dev = torch.device("cuda:0")
+    for i, (R, scale) in enumerate([(480, 1.0), (310, 50.0), (480, -3.0), (300, 0.01), (480, 1.0)]):
+        rng = np.random.default_rng(2600 + i)
+        n = 9_000 + 1_000 * i
+        host = (scale * rng.standard_normal((R, n))).astype(np.float32)
+        lens = np.full(R, n, np.int32)
+        out = gvr.topk(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev))
+        torch.cuda.synchronize()
+        _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens)
+
+
+def test_cta_timeline_diagnostic(gvr):
+    """gvr_cta_timeline records, per filter CTA, entry <= first-threshold <= exit and an SM
+    id, and per guess CTA entry <= loads arrived <= Phase 1 done <= exit."""
+    import torch
+    dev = torch.device("cuda:0")
+    R, n = 400, 20_000
+    rng = np.random.default_rng(2700)
+    host = rng.standard_normal((R, n)).astype(np.float32)
+    scores = torch.from_numpy(host).to(dev)
+    gvr.topk(scores, K)
+    torch.cuda.synchronize()
+    gvr.cta_timeline(True)
+    out = gvr.topk(scores, K)
+    ft = gvr.cta_timeline(False, "filter")
+    gt = gvr.cta_timeline(False, "guess")[:R]
+    _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K), np.full(R, n, np.int32))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ft = ft[:3 * sms]
+    ran = ft[:, 2] > 0
+    assert ran.sum() > 0
+    f = ft[ran]
+    assert np.all(f[:, 0] <= f[:, 1]) and np.all(f[:, 1] <= f[:, 2])
+    assert np.all((f[:, 3] >= 0) & (f[:, 3] < sms))
+    assert np.all(gt[:, 0] <= gt[:, 2]) and np.all(gt[:, 2] <= gt[:, 3]) and np.all(gt[:, 3] <= gt[:, 1])
+    # every filter CTA starts its stream only after some guess CTA finished
+    assert f[:, 1].min() >= gt[:, 1].min()
+
+
 # ------------------------------------------------------------------ scratch lease (ADVICE r1)
 def test_graph_captured_on_warm_stream_survives_eager_growth(gvr):
     """Warm up and capture on the SAME stream (the cache already holds a big-enough slot),

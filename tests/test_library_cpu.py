@@ -88,6 +88,11 @@ def test_argument_validation_is_synchronous(lib):
     assert lib.gvr_workspace_create(0, 10, 8, ctypes.byref(h)) == 1
     assert lib.gvr_workspace_create(1, 10, 4096, ctypes.byref(h)) == 2
     assert lib.gvr_topk_batched_host(p, 10, None, 1, None, 8, p, None, None) == 1
+    # CTA timeline diagnostic: unknown kernel id, or no output buffer when stopping
+    assert lib.gvr_cta_timeline(2, 1, None, 0, None) == 1
+    assert lib.gvr_cta_timeline(-1, 0, p, 4, None) == 1
+    assert lib.gvr_cta_timeline(0, 0, None, 4, None) == 1
+    assert lib.gvr_cta_timeline(1, 0, p, -1, None) == 1
 
 
 def test_binding_fails_loudly_without_cuda():
