@@ -243,6 +243,39 @@ __device__ __forceinline__ uint32_t group_excl_scan(G& c, uint32_t v, uint32_t& 
     return before + x - v;
 }
 
+// Exclusive scan of v plus the exclusive prefix max of m (the max of m over the threads
+// before this one, 0 for thread 0), with one barrier.
+template <class G>
+__device__ __forceinline__ uint32_t group_excl_scan_pmax(G& c, uint32_t v, uint32_t m, uint32_t& total,
+                                                         uint32_t& m_before)
+{
+    uint32_t x = v, y = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t xv = __shfl_up_sync(FULL, x, o);
+        const uint32_t yv = __shfl_up_sync(FULL, y, o);
+        if (c.lane >= o) {
+            x += xv;
+            y = max(y, yv);
+        }
+    }
+    uint32_t* s = c.red + c.par * 4 * G::W;
+    if (c.lane == 31) {
+        s[c.warp] = x;
+        s[G::W + c.warp] = y;
+    }
+    c.sync();
+    const uint32_t w = c.lane < G::W ? s[c.lane] : 0u;
+    const uint32_t wm = c.lane < G::W ? s[G::W + c.lane] : 0u;
+    const uint32_t before = __reduce_add_sync(FULL, c.lane < c.warp ? w : 0u);
+    const uint32_t mb_warps = __reduce_max_sync(FULL, c.lane < c.warp ? wm : 0u);
+    total = __reduce_add_sync(FULL, w);
+    const uint32_t mb_lanes = __shfl_up_sync(FULL, y, 1);  // inclusive max of the lanes before
+    m_before = max(mb_warps, c.lane > 0 ? mb_lanes : 0u);
+    c.par ^= 1;
+    return before + x - v;
+}
+
 // Exclusive scan of v plus the group max of m, with one barrier.
 template <class G>
 __device__ __forceinline__ uint32_t group_excl_scan_max(G& c, uint32_t v, uint32_t m, uint32_t& total, uint32_t& mall)

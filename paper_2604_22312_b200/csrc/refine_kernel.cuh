@@ -184,15 +184,21 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
         }
 #pragma unroll
         for (int i = 0; i < BPT; ++i) loc += (uint32_t)h[i];
-        uint32_t tot;
-        off0 = group_excl_scan(c, loc, tot);
+        uint32_t lmx = 0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) lmx = max(lmx, (uint32_t)h[i]);
+        uint32_t tot, mx_before;
+        off0 = group_excl_scan_pmax(c, loc, lmx, tot, mx_before);
         {
-            uint32_t off = off0;
+            // the thread holding position take-1 also knows the largest bin up to it
+            uint32_t off = off0, m = mx_before;
 #pragma unroll
             for (int i = 0; i < BPT; ++i) {
+                m = max(m, (uint32_t)h[i]);
                 if ((uint32_t)(take - 1) >= off && (uint32_t)(take - 1) < off + (uint32_t)h[i]) {
                     c.misc[12] = b0 + i;
                     c.misc[13] = (int)(off + (uint32_t)h[i]);
+                    c.misc[15] = (int)m;
                 }
                 off += (uint32_t)h[i];
             }
@@ -200,11 +206,7 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
         c.sync();
         bk = ftc >= take ? c.misc[12] : -1;
         nsel = c.misc[13];
-        uint32_t mx = 0;
-#pragma unroll
-        for (int i = 0; i < BPT; ++i)
-            if (b0 + i <= bk) mx = max(mx, (uint32_t)h[i]);
-        mx = group_red1<R_MAX>(c, mx);
+        const uint32_t mx = bk >= 0 ? (uint32_t)c.misc[15] : 0u;
         ok = bk >= 0 && nsel <= RF_CSORT && mx <= (uint32_t)CSORT_BIN_MAX;  // group-uniform
         // narrow also when the ranking would loop over bins of more than RF_BIN_FAST
         if (bk < 0 || lvl == 2 || (ok && mx <= (uint32_t)RF_BIN_FAST)) break;
@@ -250,8 +252,8 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
     // contiguous in cs in descending key order, so counting the larger composites over a
     // fixed window from the bin start (later bins and the zero padding are all smaller)
     // ranks every entry of a bin of at most RF_PAD entries without a per-compare bound.
-    for (int j = c.tid; j < nsel; j += RF_NT) {
-        const unsigned long long v = cs[j];
+    auto rank_of = [&](int j, unsigned long long& v) -> int {
+        v = cs[j];
         const int b = rbin(comp_key(v), lo, scale);
         const int cnt = hist[b];
         const int st = cur[b] - cnt;
@@ -267,10 +269,24 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
         } else {
             for (int t = 0; t < cnt; ++t) rank += cs[st + t] > v ? 1 : 0;
         }
-        const int pos = st + rank;
-        if (pos < take) {
-            o[pos] = comp_idx(v);
-            if (ov) ov[pos] = key2f(comp_key(v));
+        return st + rank;
+    };
+    if (ov) {
+        for (int j = c.tid; j < nsel; j += RF_NT) {
+            unsigned long long v;
+            const int pos = rank_of(j, v);
+            if (pos < take) {
+                o[pos] = comp_idx(v);
+                ov[pos] = key2f(comp_key(v));
+            }
+        }
+    } else {
+        for (int j = c.tid; j < nsel; j += RF_NT) {  // indices only: one predicated store
+            unsigned long long v;
+            const int pos = rank_of(j, v);
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %1, %2;\n\t@q st.global.b32 [%0], %3;\n\t}" ::"l"(o + pos),
+                         "r"(pos), "r"(take), "r"(comp_idx(v))
+                         : "memory");
         }
     }
     return true;
