@@ -1,5 +1,6 @@
 // gvr_topk.cu — C ABI of libgvrtopk.so (declared in include/gvr_topk.h): argument
 // validation, launch configuration and the host-buffer workspace entry point.
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -199,6 +200,33 @@ gvr_status set_smem(Kern kern, int bytes)
     return GVR_OK;
 }
 
+
+// The refine kernel's four instances (phase stamps on/off x the two geometries).
+gvr_status set_refine_smem()
+{
+    gvr_status st;
+    if ((st = set_smem(gvr_refine_kernel<false, RefineFew>, RF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(gvr_refine_kernel<true, RefineFew>, RF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(gvr_refine_kernel<false, RefineMany>, RF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_smem(gvr_refine_kernel<true, RefineMany>, RF_SMEM_BYTES)) != GVR_OK)
+        return st;
+    return GVR_OK;
+}
+
+// Launch the refine kernel in the geometry the batch size picks (refine_kernel.cuh):
+// go(kernel, grid, threads) performs the launch with the call's arguments.
+template <class Go>
+cudaError_t launch_refine(int64_t num_rows, int sms, bool timing, Go&& go)
+{
+    if (num_rows > RF_MANY_ROWS) {
+        const int grid = (int)std::min<int64_t>(num_rows, (int64_t)RefineMany::CPS * sms);
+        return timing ? go(gvr_refine_kernel<true, RefineMany>, grid, RefineMany::NT)
+                      : go(gvr_refine_kernel<false, RefineMany>, grid, RefineMany::NT);
+    }
+    const int grid = (int)std::min<int64_t>(num_rows, (int64_t)RefineFew::CPS * sms);
+    return timing ? go(gvr_refine_kernel<true, RefineFew>, grid, RefineFew::NT)
+                  : go(gvr_refine_kernel<false, RefineFew>, grid, RefineFew::NT);
+}
 
 gvr_status launch_status()
 {
@@ -409,8 +437,7 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
     }
     if (radix2 && (st = set_smem(radix_hist_kernel, RH_SMEM_BYTES)) != GVR_OK) return st;
     if (filt && ((st = set_smem(gvr_filter_kernel, F_SMEM_BYTES)) != GVR_OK ||
-                 (st = set_smem(gvr_refine_kernel<false>, RF_SMEM_BYTES)) != GVR_OK ||
-                 (st = set_smem(gvr_refine_kernel<true>, RF_SMEM_BYTES)) != GVR_OK ||
+                 (st = set_refine_smem()) != GVR_OK ||
                  (st = set_smem(gvr_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK))
         return st;
     ScratchLease lease;
@@ -492,9 +519,10 @@ static gvr_status gvr_launch(const float* scores, int64_t row_stride, const int3
         e = launch(gvr_filter_kernel, cl.G, F_NT, F_SMEM_BYTES, scores, row_stride, row_lens, (int)k, gpc, cl, bq);
         mark(2);
         if (e == cudaSuccess)
-            e = launch(phase_ts ? gvr_refine_kernel<true> : gvr_refine_kernel<false>, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, scores,
-                       row_stride, row_lens, (int)k,
-                       (int)num_rows, out_idx, out_val, stats, gpc, cl, bq, phase_ts, false, ctl);
+            e = launch_refine(num_rows, sms, phase_ts != nullptr, [&](auto kern, int grid, int threads) {
+                return launch(kern, grid, threads, RF_SMEM_BYTES, scores, row_stride, row_lens, (int)k, (int)num_rows,
+                              out_idx, out_val, stats, gpc, cl, bq, phase_ts, false, ctl);
+            });
         if (e == cudaSuccess)
             e = launch(gvr_fixup_kernel, min((int)num_rows, fixup_ctas), GVR_NT, GVR_SMEM_BYTES, scores, row_stride, row_lens,
                        (int)k, out_idx, out_val, stats, prm, gpc, prev_topk, phase_ts, ctl, bq);
@@ -605,7 +633,7 @@ gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32
     }
     if ((st = set_smem(indexer_guess_kernel, IXG_SMEM_BYTES)) != GVR_OK ||
         (st = set_smem(indexer_filter_kernel, IXF_SMEM_BYTES)) != GVR_OK ||
-        (st = set_smem(gvr_refine_kernel<false>, RF_SMEM_BYTES)) != GVR_OK ||
+        (st = set_refine_smem()) != GVR_OK ||
         (st = set_smem(indexer_fixup_kernel, GVR_SMEM_BYTES)) != GVR_OK)
         return st;
     // the candidate lists of the batch filter path, one filter CTA per SM
@@ -669,9 +697,10 @@ gvr_status gvr_indexer_topk_batched(const void* keys, int64_t n_max, const int32
     if (e == cudaSuccess)
         e = launch(indexer_filter_kernel, cl.G, IX_NT, IXF_SMEM_BYTES, ia, sc, row_lens, (int)k, gpc, cl, bq);
     if (e == cudaSuccess)
-        e = launch(gvr_refine_kernel<false>, min((int)num_rows, RF_CTAS_PER_SM * sms), RF_NT, RF_SMEM_BYTES, sc, n_max,
-                   row_lens, (int)k, (int)num_rows, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, gpc, cl, bq,
-                   (long long*)nullptr, true, ctl);
+        e = launch_refine(num_rows, sms, false, [&](auto kern, int grid, int threads) {
+            return launch(kern, grid, threads, RF_SMEM_BYTES, sc, n_max, row_lens, (int)k, (int)num_rows, out_idx,
+                          (float*)nullptr, (gvr_row_stats*)nullptr, gpc, cl, bq, (long long*)nullptr, true, ctl);
+        });
     if (e == cudaSuccess)
         e = launch(indexer_fixup_kernel, min((int)num_rows, sms), GVR_NT, GVR_SMEM_BYTES, ia, score_scratch, row_lens,
                    (int)k, out_idx, (float*)nullptr, (gvr_row_stats*)nullptr, prm, gpc, prev_topk, ctl, bq);

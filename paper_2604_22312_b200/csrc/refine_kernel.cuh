@@ -22,24 +22,26 @@
 
 namespace gvr {
 
-#ifndef GVR_RF_NT
-#define GVR_RF_NT 512
-#endif
-#ifndef GVR_RF_HOLD
-#define GVR_RF_HOLD 8
-#endif
-#ifndef GVR_RF_CPS
-#define GVR_RF_CPS 2
-#endif
 #ifndef GVR_RF_NBINS
 #define GVR_RF_NBINS 2048
 #endif
-constexpr int RF_NT = GVR_RF_NT;
+// (r2) Two geometries, chosen per call by the batch size (gvr_topk.cu): few rows — two
+// 512-thread CTAs per SM, 8 held entries per thread (rows finish sooner); many rows — four
+// 256-thread CTAs per SM, 16 held entries per thread (more rows in flight per SM).  Both
+// hold 4,096 list entries per row in registers at 64 registers per thread.
+template <int NT_, int HOLD_, int CPS_>
+struct RefineGeo {
+    static constexpr int NT = NT_;
+    static constexpr int HOLD = HOLD_;
+    static constexpr int CPS = CPS_;
+};
+using RefineFew = RefineGeo<512, 8, 2>;
+using RefineMany = RefineGeo<256, 16, 4>;
+constexpr int RF_MANY_ROWS = 1024;  // batches above this take RefineMany
 constexpr int RF_NBINS = GVR_RF_NBINS;  // Phase-4 bins of the refine (finer than NBINS: shorter in-bin ranking)
 constexpr int RF_CSORT = 2560;     // entries up to the K-th bin sorted in shared memory
 constexpr int RF_MAXLIST = 1 << 22;  // longest list refined here
 constexpr int RF_BIN_FAST = 16;    // largest bin ranked without narrowing first
-using RefineGroup = Group<RF_NT, 1>;
 constexpr int RF_OFF_HIST = 0;                       // int32 bin counts
 constexpr int RF_OFF_CUR = RF_OFF_HIST + RF_NBINS * 4;  // int32 bin cursors
 constexpr int RF_OFF_CS = RF_OFF_CUR + RF_NBINS * 4;
@@ -47,15 +49,13 @@ constexpr int RF_PAD = 16;    // zero composites past the sorted prefix (fixed r
 constexpr int RF_OFF_ROW = RF_OFF_CS + (RF_CSORT + RF_PAD) * 8;
 constexpr int RF_OFF_SCR = RF_OFF_ROW + 16;
 constexpr int RF_SMEM_BYTES = RF_OFF_SCR + GROUP_SCRATCH_BYTES;
-constexpr int RF_CTAS_PER_SM = GVR_RF_CPS;  // the list is held in registers (RF_HOLD slots per thread)
-static_assert(RF_CTAS_PER_SM * (RF_SMEM_BYTES + 1024) <= 233472, "refine CTAs per SM");
+static_assert(RefineMany::CPS * (RF_SMEM_BYTES + 1024) <= 233472, "refine CTAs per SM");
 
 
 // ---- Phase 4 over a row's list, instruction-lean (r2): the list is loaded once into
-// registers (RF_HOLD slots per thread: flat slot j = tid + RF_NT u of the row's
+// registers (HOLD slots per thread: flat slot j = tid + NT u of the row's
 // concatenated segments), every histogram level and the scatter run from the registers,
 // and the shared-memory atomics are predicated instead of branched around.
-constexpr int RF_HOLD = GVR_RF_HOLD;  // list entries per thread held in registers (RF_HOLD * RF_NT per row)
 
 // A row's list: its <= F_SEGS segments of the filter regions as one flat sequence.
 // tab (shared memory, written by the records step): {p_s, o_s} per segment s — the
@@ -128,20 +128,20 @@ __device__ __forceinline__ void scatter_if(int32_t* curb, unsigned long long* cs
 // that bin counting-sorted into cs as 64-bit composites and ranked inside their bins;
 // position j < take goes to o[j] / ov[j].  Returns false (group-uniform) when the row
 // cannot be finished here.  ftc = f(lo) of the first level; levels = histogram passes.
-template <class Src>
-__device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, int total, uint32_t lo, uint32_t kmax,
+template <class Geo, class Src>
+__device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& src, int total, uint32_t lo, uint32_t kmax,
                                               int take, int32_t* hist, int32_t* cur, unsigned long long* cs,
                                               int32_t* o, float* ov, int& ftc, int& levels, int& next_slot,
                                               int32_t* qhead, bool timing, long long (&ts)[TS_N])
 {
-    constexpr int BPT = RF_NBINS / RF_NT;
+    constexpr int BPT = RF_NBINS / Geo::NT;
     // held slots of this thread: u < nv
-    const int nv = total > c.tid ? min(RF_HOLD, (total - c.tid + RF_NT - 1) / RF_NT) : 0;
-    uint2 e[RF_HOLD];
+    const int nv = total > c.tid ? min(Geo::HOLD, (total - c.tid + Geo::NT - 1) / Geo::NT) : 0;
+    uint2 e[Geo::HOLD];
     {
         const auto m = src.map();
 #pragma unroll
-        for (int u = 0; u < RF_HOLD; ++u) e[u] = u < nv ? m.load(c.tid + u * RF_NT) : make_uint2(0u, 0u);
+        for (int u = 0; u < Geo::HOLD; ++u) e[u] = u < nv ? m.load(c.tid + u * Geo::NT) : make_uint2(0u, 0u);
     }
     uint32_t scale = 0u, off0 = 0u;
     const int b0 = c.tid * BPT;
@@ -160,14 +160,14 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
         scale = (uint32_t)c.misc[14];
         uint32_t f = 0;
 #pragma unroll
-        for (int u = 0; u < RF_HOLD; ++u) {
-            if (u * RF_NT >= total) break;  // group-uniform
+        for (int u = 0; u < Geo::HOLD; ++u) {
+            if (u * Geo::NT >= total) break;  // group-uniform
             const bool in = u < nv && e[u].x >= lo;
             red_inc_if(hist + rbin(e[u].x, lo, scale), in);
             f += in ? 1u : 0u;
         }
-        for (int j = c.tid + RF_HOLD * RF_NT; j < total; j += RF_NT) {  // entries past the held slots
-            const uint32_t kv = src.map().load(j).x;                       // (rare: lists > RF_HOLD RF_NT)
+        for (int j = c.tid + Geo::HOLD * Geo::NT; j < total; j += Geo::NT) {  // entries past the held slots
+            const uint32_t kv = src.map().load(j).x;                       // (rare: lists > HOLD NT)
             red_inc_if(hist + rbin(kv, lo, scale), kv >= lo);
             f += kv >= lo ? 1u : 0u;
         }
@@ -235,12 +235,12 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
     c.sync();
     // ---- counting sort of the bins up to the K-th bin (composites)
 #pragma unroll
-    for (int u = 0; u < RF_HOLD; ++u) {
-        if (u * RF_NT >= total) break;
+    for (int u = 0; u < Geo::HOLD; ++u) {
+        if (u * Geo::NT >= total) break;
         const int b = rbin(e[u].x, lo, scale);
         scatter_if(cur + b, cs, e[u].x, e[u].y, u < nv && e[u].x >= lo && b <= bk);
     }
-    for (int j = c.tid + RF_HOLD * RF_NT; j < total; j += RF_NT) {
+    for (int j = c.tid + Geo::HOLD * Geo::NT; j < total; j += Geo::NT) {
         const uint2 x = src.map().load(j);
         const int b = rbin(x.x, lo, scale);
         scatter_if(cur + b, cs, x.x, x.y, x.x >= lo && b <= bk);
@@ -272,7 +272,7 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
         return st + rank;
     };
     if (ov) {
-        for (int j = c.tid; j < nsel; j += RF_NT) {
+        for (int j = c.tid; j < nsel; j += Geo::NT) {
             unsigned long long v;
             const int pos = rank_of(j, v);
             if (pos < take) {
@@ -281,7 +281,7 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
             }
         }
     } else {
-        for (int j = c.tid; j < nsel; j += RF_NT) {  // indices only: one predicated store
+        for (int j = c.tid; j < nsel; j += Geo::NT) {  // indices only: one predicated store
             unsigned long long v;
             const int pos = rank_of(j, v);
             asm volatile("{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %1, %2;\n\t@q st.global.b32 [%0], %3;\n\t}" ::"l"(o + pos),
@@ -292,8 +292,8 @@ __device__ __forceinline__ bool refine_phase4(RefineGroup& c, const Src& src, in
     return true;
 }
 
-template <bool TIMING>
-__global__ void __launch_bounds__(RF_NT, RF_CTAS_PER_SM)
+template <bool TIMING, class Geo>
+__global__ void __launch_bounds__(Geo::NT, Geo::CPS)
 gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_t* __restrict__ row_lens, int k,
                   int num_rows, int32_t* out, float* out_val, gvr_row_stats* stats, const GuessOut* gp, CandLists cl,
                   BatchQueue bq, long long* phase_ts, bool fused = false, int32_t* ctl = nullptr)
@@ -310,7 +310,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
     int32_t* cur = reinterpret_cast<int32_t*>(smem + RF_OFF_CUR);
     unsigned long long* cs = reinterpret_cast<unsigned long long*>(smem + RF_OFF_CS);
     int* sh_row = reinterpret_cast<int*>(smem + RF_OFF_ROW);
-    RefineGroup c;
+    Group<Geo::NT, 1> c;
     c.init(threadIdx.x, smem + RF_OFF_SCR);
     const int K = k;
     // thread 0 claims the next queue slot during the current row's last step (ranking),
@@ -402,7 +402,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         if (trivial && fused) ok = false;
         if (trivial && !fused) {
             uint32_t mn = 0xffffffffu, mx2 = 0u;
-            for (int q = c.tid; q < p.n; q += RF_NT) {
+            for (int q = c.tid; q < p.n; q += Geo::NT) {
                 const uint32_t kv = f2key(__ldg(p.x + q));
                 mn = min(mn, kv);
                 mx2 = max(mx2, kv);
@@ -421,14 +421,14 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             int32_t* o = out + (int64_t)r * k;
             float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
             if (rowx) {
-                ok = refine_phase4(c, RowSrc{rowx}, total, Tc, kmax, take, hist, cur, cs, o, ov, ftc, levels,
+                ok = refine_phase4<Geo>(c, RowSrc{rowx}, total, Tc, kmax, take, hist, cur, cs, o, ov, ftc, levels,
                                    next_slot, bq.qctl + Q_HEAD, timing, tsr);
             } else {
-                ok = refine_phase4(c, ListSrc{cl.region, c.misc + 24}, total, Tc, kmax, take, hist, cur, cs, o, ov, ftc, levels, next_slot,
+                ok = refine_phase4<Geo>(c, ListSrc{cl.region, c.misc + 24}, total, Tc, kmax, take, hist, cur, cs, o, ov, ftc, levels, next_slot,
                                    bq.qctl + Q_HEAD, timing, tsr);
             }
             if (ok && !tie_fill)
-                for (int j = take + c.tid; j < k; j += RF_NT) {  // len < k: -1 padding
+                for (int j = take + c.tid; j < k; j += Geo::NT) {  // len < k: -1 padding
                     o[j] = -1;
                     if (ov) ov[j] = 0.f;
                 }
@@ -442,7 +442,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
             float* ov = out_val ? out_val + (int64_t)r * k : nullptr;
             const int need = K - take;
             int found = 0;
-            for (int base = 0; base < p.n && found < need; base += 8 * RF_NT) {
+            for (int base = 0; base < p.n && found < need; base += 8 * Geo::NT) {
                 const int i0 = base + 8 * c.tid;
                 uint32_t hit = 0u;
 #pragma unroll
@@ -463,7 +463,7 @@ gvr_refine_kernel(const float* __restrict__ scores, int64_t stride, const int32_
         }
         if (trivial && p.n == 0 && !fused) {
             int32_t* o = out + (int64_t)r * k;
-            for (int j = c.tid; j < k; j += RF_NT) {
+            for (int j = c.tid; j < k; j += Geo::NT) {
                 o[j] = -1;
                 if (out_val) out_val[(int64_t)r * k + j] = 0.f;
             }
