@@ -618,6 +618,30 @@ def test_filter_path_alternating_batch_sizes_and_paths(gvr):
         _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens)
 
 
+@pytest.mark.parametrize("R", [400, 1100])
+def test_refine_lists_longer_than_the_held_registers(gvr, R):
+    """Both refine geometries (R <= 1024: 512 threads x 8 held entries; R > 1024: 256 x 16)
+    hold 4,096 list entries per row in registers and re-read the rest from L2 on every
+    pass.  A wide Phase-2 window (window_z = 30) lowers T_c until most lists exceed 4,096
+    entries: exact; the rows refined from their lists had more than 4,096 candidates."""
+    import torch
+    dev = torch.device("cuda:0")
+    n = 30_000
+    rng = np.random.default_rng(2800 + R)
+    host = rng.standard_normal((R, n)).astype(np.float32)
+    lens = np.full(R, n, np.int32)
+    out, _, st = gvr.topk_ex(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev),
+                             options=gvr.GvrOptions(30.0, 0, 0, 0, 0))
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens, st)
+    # most rows were refined from lists longer than the held capacity, in one HBM pass (at
+    # R = 1100 some CTA regions overflow: those rows are streamed again by the fixup — exact)
+    long_rows = st[:, 2] > 4096
+    assert long_rows.mean() > 0.5, np.percentile(st[:, 2], [0, 50, 100])
+    assert (st[long_rows, 4] == 1).all()
+
+
 def test_threshold_handoff_never_reads_a_stale_generation(gvr):
     """The filter kernel takes each row's T_c from a generation-tagged word (BatchQueue::tcw)
     instead of waiting for the guess grid.  Rows of a shrinking then growing batch on one
