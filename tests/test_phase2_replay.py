@@ -67,19 +67,19 @@ def test_window_cfg2_values():
 
 # --------------------------------------------------------------------------- sample layout
 def test_sample_positions_layout():
-    """64 runs of 64 contiguous floats, run g at head + 64 floor(g nrun / 64); thread c
-    reads the 16 floats at 16 (c % 4) inside run c // 4 (DESIGN.md R34)."""
+    """128 runs of 32 contiguous floats, run g at head + 32 floor(g nrun / 128); thread c
+    reads the 16 floats at 16 (c % 2) inside run c // 2 (DESIGN.md R34)."""
     n, head = 100_003, 3
     pos = P2.sample_positions(n, head)
     assert pos.size == 4096 and len(np.unique(pos)) == 4096
-    nrun = (4 * ((n - head) // 4)) // 64
-    for g in (0, 1, 33, 63):
-        start = head + 64 * ((g * nrun) // 64)
-        assert list(pos[64 * g:64 * g + 64]) == list(range(start, start + 64))
+    nrun = (4 * ((n - head) // 4)) // 32
+    for g in (0, 1, 77, 127):
+        start = head + 32 * ((g * nrun) // 128)
+        assert list(pos[32 * g:32 * g + 32]) == list(range(start, start + 32))
     assert pos.max() < n and pos.min() == head
-    # runs are spread over the row: consecutive runs start nrun // 64 runs apart (or one more)
-    gaps = np.diff(pos[::64])
-    assert set(gaps) <= {64 * (nrun // 64), 64 * (nrun // 64 + 1)}
+    # runs are spread over the row: consecutive runs start nrun // 128 runs apart (or one more)
+    gaps = np.diff(pos[::32])
+    assert set(gaps) <= {32 * (nrun // 128), 32 * (nrun // 128 + 1)}
 
 
 # --------------------------------------------------------------------------- Phase 1
