@@ -25,8 +25,8 @@ import numpy as np
 SAMPLE_CHUNKS = 256        # 16-float chunks per row sample (one per guess-kernel thread)
 CHUNK = 16                 # floats per chunk (one 64-byte read)
 S = SAMPLE_CHUNKS * CHUNK  # 4096 sample values
-RUN = 32                   # floats per contiguous sample run (R34): 2 chunks
-NRUN = S // RUN            # 128 runs per row sample
+RUN = 16                   # floats per contiguous sample run (R34): one chunk
+NRUN = S // RUN            # 256 runs per row sample
 Z = np.float32(4.5)        # window lower edge: mu + Z sqrt(mu) sample hits (R35)
 MAX_SECANT = 8             # secant steps before pure bisection (R11)
 MAX_ITERS = 12             # count evaluations before the Phase-2 fallback (R12)
@@ -55,10 +55,10 @@ def keys(a: np.ndarray) -> np.ndarray:
 
 
 def sample_positions(n: int, head: int) -> np.ndarray:
-    """Row positions of the sample, in guess-kernel thread order (R34): 128 runs of
-    32 contiguous floats, run g at head + 32 * floor(g * nrun / 128) with nrun = floor(body /
-    32) runs of the 16-byte aligned body (head = scalars before the first 16-byte boundary);
-    chunk c (thread c, c < 256) is the 16 floats at 16 * (c % 2) inside run c // 2."""
+    """Row positions of the sample, in guess-kernel thread order (R34): 256 runs of
+    16 contiguous floats, run g (thread g's chunk) at head + 16 * floor(g * nrun / 256) with
+    nrun = floor(body / 16) runs of the 16-byte aligned body (head = scalars before the
+    first 16-byte boundary)."""
     body = 4 * ((n - head) // 4)
     nrun = body // RUN
     c = np.arange(SAMPLE_CHUNKS, dtype=np.int64)

@@ -660,7 +660,7 @@ __device__ __forceinline__ float group_fsum1(G& c, float a)
 constexpr int P2_CHUNK = 16;                 // sample floats per thread (one 64-byte read)
 constexpr int P2_S = 256 * P2_CHUNK;         // sample values: one chunk per thread
 #ifndef GVR_P2_RUN
-#define GVR_P2_RUN 32
+#define GVR_P2_RUN 16
 #endif
 constexpr int P2_RUN = GVR_P2_RUN;           // floats per contiguous sample run (P2_RUN / 16 threads)
 constexpr int P2_TPR = P2_RUN / P2_CHUNK;    // threads per run
@@ -685,7 +685,7 @@ constexpr float P2_Z_DEFAULT = 4.5f;
 //     -> pmin / pmax (keys), pmean = sum / count (Eq. 4).
 //     No valid guess -> the statistics of the row sample.
 //   Sample: thread t's 16 contiguous floats of the 16-byte aligned body at sample_off(t):
-//     128 runs of 32 floats spread over the row (R34), in registers, as keys.
+//     256 chunks of 16 floats spread over the row (R34), in registers, as keys.
 //   Phase 2: window [L, H] in sample hits, L = ceil(mu + z sqrt(mu)) with mu = k S / n
 //     the expected hits at the K-th value, H = L + ceil(L / 2), target (L + H) / 2;
 //     anchors exact for the sample: (min key, S), (max key + 1, 0) (R8).  Probe T0 =

@@ -240,7 +240,7 @@ __device__ __forceinline__ void score_tiles(const QFrag& f, uint32_t kbuf, const
 
 // ---------------------------------------------------------------------------------
 // Fused Phases 1-2 (gvr_indexer_topk_batched): one CTA per row computes the scores at the
-// guessed positions and at the 4096 row-sample positions (sample_off: 128 runs of 32
+// guessed positions and at the 4096 row-sample positions (sample_off: 256 chunks of 16
 // consecutive keys spread over the row — the score path's sample with head 0)
 // and runs phase12_core on them.  Rows with no tiles go to the ready queue.
 constexpr int IXG_OFF_Q = 0;

@@ -67,19 +67,18 @@ def test_window_cfg2_values():
 
 # --------------------------------------------------------------------------- sample layout
 def test_sample_positions_layout():
-    """128 runs of 32 contiguous floats, run g at head + 32 floor(g nrun / 128); thread c
-    reads the 16 floats at 16 (c % 2) inside run c // 2 (DESIGN.md R34)."""
+    """256 chunks of 16 contiguous floats, chunk c (thread c) at head + 16 floor(c nrun / 256)
+    (R34)."""
     n, head = 100_003, 3
     pos = P2.sample_positions(n, head)
     assert pos.size == 4096 and len(np.unique(pos)) == 4096
-    nrun = (4 * ((n - head) // 4)) // 32
-    for g in (0, 1, 77, 127):
-        start = head + 32 * ((g * nrun) // 128)
-        assert list(pos[32 * g:32 * g + 32]) == list(range(start, start + 32))
+    nrun = (4 * ((n - head) // 4)) // 16
+    for c in (0, 1, 100, 255):
+        start = head + 16 * ((c * nrun) // 256)
+        assert list(pos[16 * c:16 * c + 16]) == list(range(start, start + 16))
     assert pos.max() < n and pos.min() == head
-    # runs are spread over the row: consecutive runs start nrun // 128 runs apart (or one more)
-    gaps = np.diff(pos[::32])
-    assert set(gaps) <= {32 * (nrun // 128), 32 * (nrun // 128 + 1)}
+    gaps = np.diff(pos[::16])
+    assert set(gaps) <= {16 * (nrun // 256), 16 * (nrun // 256 + 1)}
 
 
 # --------------------------------------------------------------------------- Phase 1
