@@ -42,6 +42,7 @@ constexpr int RF_NBINS = GVR_RF_NBINS;  // Phase-4 bins of the refine (finer tha
 constexpr int RF_CSORT = 2560;     // entries up to the K-th bin sorted in shared memory
 constexpr int RF_MAXLIST = 1 << 22;  // longest list refined here
 constexpr int RF_BIN_FAST = 16;    // largest bin ranked without narrowing first
+constexpr int RF_ZOOM_MIN = 64;    // a lowest K-th bin above this is zoomed into from above
 constexpr int RF_OFF_HIST = 0;                       // int32 bin counts
 constexpr int RF_OFF_CUR = RF_OFF_HIST + RF_NBINS * 4;  // int32 bin cursors
 constexpr int RF_OFF_CS = RF_OFF_CUR + RF_NBINS * 4;
@@ -102,7 +103,8 @@ __device__ __forceinline__ uint32_t rf_scale(uint64_t range)
 // Descending linear bin of key >= lo over [lo, lo + range): bin 0 holds the largest keys.
 __device__ __forceinline__ int rbin(uint32_t key, uint32_t lo, uint32_t scale)
 {
-    return (RF_NBINS - 1) - min((int)__umulhi(key - lo, scale), RF_NBINS - 1);
+    // (unsigned clamp: after a zoom, keys far above the binned range give products >= 2^31)
+    return (RF_NBINS - 1) - (int)min(__umulhi(key - lo, scale), (uint32_t)(RF_NBINS - 1));
 }
 __device__ __forceinline__ void red_inc_if(int32_t* p, bool pred)
 {
@@ -144,6 +146,7 @@ __device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& s
         for (int u = 0; u < Geo::HOLD; ++u) e[u] = u < nv ? m.load(c.tid + u * Geo::NT) : make_uint2(0u, 0u);
     }
     uint32_t scale = 0u, off0 = 0u;
+    uint32_t hi = kmax;  // binned range [lo, hi]; keys above hi saturate into bin 0
     const int b0 = c.tid * BPT;
     int h[BPT];
     int bk = -1, nsel = 0;
@@ -154,7 +157,7 @@ __device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& s
         for (int i = 0; i < BPT / 4; ++i) reinterpret_cast<int4*>(hist + b0)[i] = make_int4(0, 0, 0, 0);
         if (c.tid == 0) {
             c.misc[12] = -1;  // K-th bin: set below by the thread that holds it
-            c.misc[14] = (int)rf_scale((uint64_t)kmax - lo + 1ull);  // one 64-bit division per level
+            c.misc[14] = (int)rf_scale((uint64_t)hi - lo + 1ull);  // one 64-bit division per level
         }
         c.sync();
         scale = (uint32_t)c.misc[14];
@@ -199,6 +202,7 @@ __device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& s
                     c.misc[12] = b0 + i;
                     c.misc[13] = (int)(off + (uint32_t)h[i]);
                     c.misc[15] = (int)m;
+                    c.misc[16] = h[i];
                 }
                 off += (uint32_t)h[i];
             }
@@ -213,7 +217,17 @@ __device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& s
         // lower edge of bin bk: the smallest d with floor(d scale / 2^32) = RF_NBINS - 1 - bk
         const uint64_t L = (uint64_t)(RF_NBINS - 1 - bk);
         const uint64_t dmin = ((L << 32) + scale - 1ull) / scale;
-        if (dmin == 0ull) break;  // the K-th bin is the lowest: narrowing cannot help
+        if (dmin == 0ull) {
+            // the K-th bin is the lowest.  Moderately crowded: ranked as it is.  Heavily
+            // crowded (a few keys far above the rest stretch the range): zoom into that bin
+            // from above (its top edge becomes hi; the keys above saturate into bin 0)
+            // (only when the keys above that bin are few: they all land in bin 0)
+            if (mx <= (uint32_t)RF_ZOOM_MIN || nsel - c.misc[16] > RF_PAD) break;
+            const uint64_t dtop = ((1ull << 32) + scale - 1ull) / scale;  // first d of the next bin up
+            if (dtop <= 1ull) break;
+            hi = lo + (uint32_t)(dtop - 1ull);
+            continue;
+        }
         lo += (uint32_t)dmin;
     }
     if (timing) ts[TS_PHASE23] = clock64();

@@ -642,6 +642,28 @@ def test_refine_lists_longer_than_the_held_registers(gvr, R):
     assert (st[long_rows, 4] == 1).all()
 
 
+def test_refine_zooms_into_a_crowded_lowest_bin(gvr):
+    """Rows whose candidate list is a dense cluster of negative scores plus a few far
+    positive outliers: in linear key bins over [T_c, max] nearly every entry falls into the
+    lowest bin, which is also the K-th bin.  The refine zooms into that bin from above
+    (the outliers saturate into bin 0) instead of ranking thousands of entries in one
+    bin: exact, refined from the lists, three histogram levels."""
+    import torch
+    dev = torch.device("cuda:0")
+    R, n = 320, 30_000
+    rng = np.random.default_rng(2900)
+    host = (-1.0 + 1e-3 * rng.standard_normal((R, n))).astype(np.float32)
+    for r in range(R):
+        host[r, rng.choice(n, 12, replace=False)] = (100.0 + 50 * rng.random(12)).astype(np.float32)
+    lens = np.full(R, n, np.int32)
+    out, _, st = gvr.topk_ex(torch.from_numpy(host).to(dev), K, row_lens=torch.from_numpy(lens).to(dev))
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    _assert_rows(out.cpu().numpy(), oracle.topk_batched(host, K, row_lens=lens), lens, st)
+    assert (st[:, 5] >= 1).mean() > 0.9, np.bincount(st[:, 5])  # narrowed / zoomed
+    assert (st[:, 1] == 0).all()  # no row needed the fixup kernel (its snap iterations)
+
+
 def test_threshold_handoff_never_reads_a_stale_generation(gvr):
     """The filter kernel takes each row's T_c from a generation-tagged word (BatchQueue::tcw)
     instead of waiting for the guess grid.  Rows of a shrinking then growing batch on one
