@@ -18,6 +18,9 @@
 // Phase 2 (the secant search) ran in gvr_guess_kernel over the row
 // sample, so the list is {key >= T_c} with K <= f(T_c) ~ 1.3-2 K (R34-R36).
 #pragma once
+#ifdef GVR_DEBUG_BOUNDS
+#include <cstdio>
+#endif
 #include "filter_kernel.cuh"
 
 namespace gvr {
@@ -166,6 +169,12 @@ __device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& s
         for (int u = 0; u < Geo::HOLD; ++u) {
             if (u * Geo::NT >= total) break;  // group-uniform
             const bool in = u < nv && e[u].x >= lo;
+#ifdef GVR_DEBUG_BOUNDS  // debug builds: every bin in range (nvcc -DGVR_DEBUG_BOUNDS)
+            if (in && (rbin(e[u].x, lo, scale) < 0 || rbin(e[u].x, lo, scale) >= RF_NBINS)) {
+                printf("refine: bin out of range, lo %u hi %u scale %u key %u\n", lo, hi, scale, e[u].x);
+                __trap();
+            }
+#endif
             red_inc_if(hist + rbin(e[u].x, lo, scale), in);
             f += in ? 1u : 0u;
         }
@@ -260,6 +269,18 @@ __device__ __forceinline__ bool refine_phase4(Group<Geo::NT, 1>& c, const Src& s
         scatter_if(cur + b, cs, x.x, x.y, x.x >= lo && b <= bk);
     }
     c.sync();
+#ifdef GVR_DEBUG_BOUNDS  // debug builds: the scatter filled every bin up to the K-th exactly
+    {
+        int off = (int)off0;
+        for (int i = 0; i < BPT; ++i) {
+            if (b0 + i <= bk && cur[b0 + i] != off + h[i]) {
+                printf("refine: bin %d filled to %d, expected %d\n", b0 + i, cur[b0 + i], off + h[i]);
+                __trap();
+            }
+            off += h[i];
+        }
+    }
+#endif
     if (timing) ts[TS_PHASE4] = clock64();
     if (c.tid == 0 && qhead) next_slot = atomicAdd(qhead, 1);
     // ---- rank inside the bin; positions < take are the ordered output.  Bins are
